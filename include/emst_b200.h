@@ -1,0 +1,140 @@
+/*
+ * emst_b200.h -- C ABI of the B200-native single-tree Boruvka EMST.
+ *
+ * Plain pointers and sizes only (no torch / numpy types).  Each entry point
+ * replaces one function of the reference package (/root/reference/pkg/src/emst);
+ * the citation next to it is the reference interface it stands in for.  The
+ * Python drop-in (paper_2207_00514_b200/) binds these with ctypes, see
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *   - points are row-major float32 (n, d), d in {2, 3}; every output array is
+ *     caller-allocated with the documented size.
+ *   - EMST_POINTS_ON_DEVICE: `pts` is a CUDA device pointer (zero-copy hand-off
+ *     of a contiguous float32 CUDA tensor); otherwise a host pointer.
+ *   - EMST_OUTPUT_ON_DEVICE: edges/weights outputs are device pointers.
+ *   - every call returns an emst_status; on failure `err` (if non-NULL) holds a
+ *     NUL-terminated message.  No call falls back to the CPU.
+ *   - a context is bound to one CUDA device and one stream; calls on one context
+ *     must be serialised by the caller (the Python layer holds a lock).
+ */
+#ifndef EMST_B200_H
+#define EMST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum emst_status {
+  EMST_OK = 0,
+  EMST_ERR_EMPTY = 1,          /* EmptyDatasetError          (geometry.py:64-65)   */
+  EMST_ERR_DIM = 2,            /* UnsupportedDimensionError  (geometry.py:59-67)   */
+  EMST_ERR_NONFINITE = 3,      /* InvalidCoordinateError     (geometry.py:68-70)   */
+  EMST_ERR_STACK = 4,          /* TraversalStackOverflowError (mst.py:705-707)     */
+  EMST_ERR_NO_EDGE = 5,        /* InternalInvariantViolation (mst.py:720-721)      */
+  EMST_ERR_CHAIN = 6,          /* InternalInvariantViolation (mst.py:722-723)      */
+  EMST_ERR_NO_REDUCE = 7,      /* InternalInvariantViolation (mst.py:724-725)      */
+  EMST_ERR_ITER = 8,           /* InternalInvariantViolation (mst.py:682-684)      */
+  EMST_ERR_COUNT = 9,          /* InternalInvariantViolation (mst.py:742-744)      */
+  EMST_ERR_CUDA = 10,          /* DeviceError (new)                                */
+  EMST_ERR_NCCL = 11,          /* DeviceError (new)                                */
+  EMST_ERR_PARAM = 12,         /* InvalidParameterError                            */
+  EMST_ERR_TOO_LARGE = 13,     /* InvalidParameterError: n beyond 2^30 - 1         */
+  EMST_ERR_NOTHING = 14,       /* NothingToFindError         (mst.py:487-488)      */
+  EMST_ERR_MISSING = 15        /* NoOutgoingEdgeError        (mst.py:510-513)      */
+} emst_status;
+
+enum {
+  EMST_SUBTREE_SKIP = 1,        /* boruvka_emst(subtree_skip=True)        mst.py:579 */
+  EMST_UPPER_BOUNDS = 2,        /* boruvka_emst(upper_bound_seeding=True) mst.py:580 */
+  EMST_POINTS_ON_DEVICE = 4,
+  EMST_OUTPUT_ON_DEVICE = 8
+};
+
+/* Phase slots of emst_stats.phase_ms, the keys of MstResult.phase_timings (mst.py:756-765). */
+enum {
+  EMST_PHASE_TREE = 0, EMST_PHASE_CORE = 1, EMST_PHASE_REDUCE_LABELS = 2, EMST_PHASE_UPPER_BOUNDS = 3,
+  EMST_PHASE_FIND_EDGES = 4, EMST_PHASE_MERGE = 5, EMST_PHASE_MST = 6, EMST_PHASE_TOTAL = 7
+};
+
+/* Run instrumentation, the non-array fields of MstResult (mst.py:158-182). */
+typedef struct emst_stats {
+  int32_t iterations;
+  int32_t num_counts;
+  int64_t component_counts[64];
+  int64_t leaf_distance_evals;
+  double phase_ms[8];
+  int64_t bad_row;              /* first non-finite row when EMST_ERR_NONFINITE */
+  int64_t kernel_launches;      /* kernels this call launched */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+  int32_t world;                /* GPUs that shared the traversal */
+  int32_t rank;
+} emst_stats;
+
+typedef struct emst_context emst_context;
+
+/* NCCL rendezvous id (128 bytes) for a multi-GPU context; rank 0 creates it and
+ * the caller broadcasts it (torch.distributed in the Python layer). */
+int emst_nccl_unique_id(void* id_out_128, char* err, size_t errlen);
+
+/* One context per (process, device).  world > 1 shares every Boruvka round's
+ * traversal by Morton slot range over `world` ranks (replicated tree, one
+ * two-phase NCCL min-reduction per round); nccl_id may be NULL when world == 1. */
+int emst_context_create(int device, int rank, int world, const void* nccl_id, emst_context** out,
+                        char* err, size_t errlen);
+int emst_context_destroy(emst_context* ctx);
+
+/* Single-GPU shard emulation: split each round's traversal into `shards` Morton
+ * ranges and combine them with the same two-phase min protocol the NCCL path
+ * uses (for determinism tests of the multi-GPU protocol on one device). */
+int emst_context_set_virtual_shards(emst_context* ctx, int shards);
+
+/* boruvka_emst(points, "euclidean", 1, subtree_skip, upper_bound_seeding)
+ * (mst.py:578-769).  edges_out: (n-1) x 2 int64, u < v; weights_out: (n-1)
+ * float64; rows sorted by (weight, u, v).  stats may be NULL. */
+int emst_boruvka(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags,
+                 int64_t* edges_out, double* weights_out, emst_stats* stats, char* err, size_t errlen);
+
+/* morton_codes(points) with the tight scene bounds (geometry.py:209-227). codes_out: n u64 (host). */
+int emst_morton_codes(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags,
+                      uint64_t* codes_out, char* err, size_t errlen);
+
+/* build(points) (bvh.py:305-340) in the reference's array layout (bvh.py:39-75):
+ * perm n, left/right/parent n-1, leaf_parent n (int64); box_lo/box_hi (n-1) x d f32. Host outputs. */
+int emst_build(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t* perm,
+               int64_t* left, int64_t* right, int64_t* parent, int64_t* leaf_parent, float* box_lo,
+               float* box_hi, char* err, size_t errlen);
+
+/* reduce_labels(build(points), state) (mst.py:436-448): labels n int64 (point order) -> internal labels n-1. */
+int emst_reduce_labels(emst_context* ctx, const float* pts, int64_t n, int32_t d, const int64_t* labels,
+                       int64_t* internal_labels, char* err, size_t errlen);
+
+/* compute_upper_bounds(state, build(points).leaf_perm, points) (mst.py:451-469): ub_out n f64 by label. */
+int emst_compute_upper_bounds(emst_context* ctx, const float* pts, int64_t n, int32_t d, const int64_t* labels,
+                              double* ub_out, char* err, size_t errlen);
+
+/* find_component_outgoing_edges (mst.py:472-514): per-label best edge arrays (n each, -1 / inf
+ * where none), flags as emst_boruvka; ub is read only with EMST_UPPER_BOUNDS. */
+int emst_find_component_outgoing_edges(emst_context* ctx, const float* pts, int64_t n, int32_t d,
+                                       const int64_t* labels, const double* ub, int32_t flags, int64_t* best_u,
+                                       int64_t* best_v, double* best_w, int64_t* leaf_evals, char* err,
+                                       size_t errlen);
+
+/* merge_components (mst.py:517-547): reps (s, ascending), per-label best arrays (n); labels
+ * (n) relabelled in place; out_u/out_v/out_w (s) and new_reps (s) with their counts. */
+int emst_merge_components(emst_context* ctx, int64_t n, const int64_t* reps, int64_t s, const int64_t* best_u,
+                          const int64_t* best_v, const double* best_w, int64_t* labels, int64_t* out_u,
+                          int64_t* out_v, double* out_w, int64_t* n_edges, int64_t* new_reps, int64_t* n_new,
+                          char* err, size_t errlen);
+
+/* Library identification: compiled arch string (e.g. "sm_100a") and a build tag. */
+const char* emst_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EMST_B200_H */

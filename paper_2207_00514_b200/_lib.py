@@ -1,0 +1,219 @@
+"""ctypes binding of the native library ``libemst_b200.so`` (C ABI: include/emst_b200.h).
+
+There is no CPU fallback: if the library is missing, fails to load, or no CUDA
+device is present, every compute call raises :class:`~.errors.DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+from .errors import (
+    DeviceError,
+    EmptyDatasetError,
+    InternalInvariantViolation,
+    InvalidCoordinateError,
+    InvalidParameterError,
+    NoOutgoingEdgeError,
+    NothingToFindError,
+    TraversalStackOverflowError,
+    UnsupportedDimensionError,
+)
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libemst_b200.so")
+CSRC = os.path.join(PKG_DIR, "csrc")
+
+SUBTREE_SKIP = 1
+UPPER_BOUNDS = 2
+POINTS_ON_DEVICE = 4
+OUTPUT_ON_DEVICE = 8
+
+PHASES = ("tree", "core", "reduce_labels", "upper_bounds", "find_edges", "merge", "mst", "total")
+
+# emst_status -> exception class (include/emst_b200.h)
+_STATUS = {
+    1: EmptyDatasetError,
+    2: UnsupportedDimensionError,
+    3: InvalidCoordinateError,
+    4: TraversalStackOverflowError,
+    5: InternalInvariantViolation,
+    6: InternalInvariantViolation,
+    7: InternalInvariantViolation,
+    8: InternalInvariantViolation,
+    9: InternalInvariantViolation,
+    10: DeviceError,
+    11: DeviceError,
+    12: InvalidParameterError,
+    13: InvalidParameterError,
+    14: NothingToFindError,
+    15: NoOutgoingEdgeError,
+}
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [
+        ("iterations", ctypes.c_int32),
+        ("num_counts", ctypes.c_int32),
+        ("component_counts", ctypes.c_int64 * 64),
+        ("leaf_distance_evals", ctypes.c_int64),
+        ("phase_ms", ctypes.c_double * 8),
+        ("bad_row", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+        ("h2d_bytes", ctypes.c_int64),
+        ("d2h_bytes", ctypes.c_int64),
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+    ]
+
+
+EXPORTS = (
+    "emst_nccl_unique_id",
+    "emst_context_create",
+    "emst_context_destroy",
+    "emst_context_set_virtual_shards",
+    "emst_boruvka",
+    "emst_morton_codes",
+    "emst_build",
+    "emst_reduce_labels",
+    "emst_compute_upper_bounds",
+    "emst_find_component_outgoing_edges",
+    "emst_merge_components",
+    "emst_build_info",
+)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def build(verbose: bool = False) -> str:
+    """Compile the CUDA library in-tree for sm_100a (nvcc cross-compiles without a GPU)."""
+    cmd = ["make", "-C", CSRC]
+    if not verbose:
+        cmd.insert(1, "-s")
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+def load():
+    """Load and type the native library (raises DeviceError if it is absent)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(f"native library {LIB_PATH} is missing; run __graft_entry__.build() "
+                              "(make -C paper_2207_00514_b200/csrc)")
+        try:
+            L = ctypes.CDLL(LIB_PATH)
+        except OSError as exc:
+            raise DeviceError(f"cannot load {LIB_PATH}: {exc}") from exc
+        vp, i64, i32, cp, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_char_p, ctypes.c_size_t
+        L.emst_nccl_unique_id.argtypes = [vp, cp, sz]
+        L.emst_context_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(vp), cp, sz]
+        L.emst_context_destroy.argtypes = [vp]
+        L.emst_context_set_virtual_shards.argtypes = [vp, ctypes.c_int]
+        L.emst_boruvka.argtypes = [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(Stats), cp, sz]
+        L.emst_morton_codes.argtypes = [vp, vp, i64, i32, i32, vp, cp, sz]
+        L.emst_build.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, cp, sz]
+        L.emst_reduce_labels.argtypes = [vp, vp, i64, i32, vp, vp, cp, sz]
+        L.emst_compute_upper_bounds.argtypes = [vp, vp, i64, i32, vp, vp, cp, sz]
+        L.emst_find_component_outgoing_edges.argtypes = [vp, vp, i64, i32, vp, vp, i32, vp, vp, vp, vp, cp, sz]
+        L.emst_merge_components.argtypes = [vp, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, cp, sz]
+        L.emst_build_info.restype = ctypes.c_char_p
+        for name in EXPORTS:
+            getattr(L, name).restype = ctypes.c_int if name != "emst_build_info" else ctypes.c_char_p
+        _lib = L
+        return L
+
+
+def raise_for(code: int, err: ctypes.Array, stats: Stats | None = None):
+    if code == 0:
+        return
+    msg = err.value.decode(errors="replace") if err is not None else f"status {code}"
+    exc = _STATUS.get(code, DeviceError)
+    raise exc(msg)
+
+
+def err_buf():
+    return ctypes.create_string_buffer(512)
+
+
+def ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+class Context:
+    """One native context: a CUDA device, its stream and workspace, optionally an NCCL rank."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+        L = load()
+        h = ctypes.c_void_p()
+        e = err_buf()
+        idbuf = ctypes.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        rc = L.emst_context_create(int(device), int(rank), int(world), idbuf, ctypes.byref(h), e, len(e))
+        raise_for(rc, e)
+        self.handle = h
+        self.device, self.rank, self.world = int(device), int(rank), int(world)
+        self.lock = threading.Lock()
+
+    def set_virtual_shards(self, shards: int) -> None:
+        rc = load().emst_context_set_virtual_shards(self.handle, int(shards))
+        if rc:
+            raise InvalidParameterError(f"virtual shard count {shards} out of range [1, 64]")
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            load().emst_context_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    L = load()
+    buf = ctypes.create_string_buffer(128)
+    e = err_buf()
+    raise_for(L.emst_nccl_unique_id(buf, e, len(e)), e)
+    return buf.raw
+
+
+_default: dict[int, Context] = {}
+
+
+def default_context(device: int | None = None) -> Context:
+    """Process-wide single-GPU context for `device` (current CUDA device by default)."""
+    if device is None:
+        device = _current_device()
+    with _lock:
+        ctx = _default.get(device)
+    if ctx is None:
+        ctx = Context(device)
+        with _lock:
+            _default.setdefault(device, ctx)
+            ctx = _default[device]
+    return ctx
+
+
+def set_default_context(ctx: Context) -> None:
+    with _lock:
+        _default[ctx.device] = ctx
+
+
+def _current_device() -> int:
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.cuda.current_device()
+    except Exception:
+        pass
+    return 0

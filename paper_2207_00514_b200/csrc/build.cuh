@@ -1,0 +1,294 @@
+// build.cuh -- LBVH construction kernels (reference: geometry.py, bvh.py:305-340).
+//
+//   k_scene         bounds + finiteness in one read of the points; the last block
+//                   folds the per-block partials and derives lo / 1/extent in f64
+//                   (geometry.py:36-71, 102-105, 201-206)
+//   k_morton        bit-exact quantise + interleave (geometry.py:143-227)
+//   (radix sort)    stable Z-order permutation (bvh.py:317)
+//   k_gather        float4 points in slot order, perm / iperm as u32
+//   k_karras        radix-tree topology, node numbering identical to the
+//                   reference's _build_topology (bvh.py:112-201)
+//   k_refit         bottom-up boxes by atomic-arrival climb: the second thread to
+//                   reach a node combines its children (replaces the serial level
+//                   schedule of bvh.py:204-264, 293-302)
+#pragma once
+#include "common.cuh"
+
+namespace emst {
+
+struct Scene {
+  double lo[3];
+  double inv[3];
+  float flo[3];
+  float fhi[3];
+  long long bad_row;     // first row holding a non-finite coordinate, or LLONG_MAX
+  unsigned blocks_done;
+  int pad;
+};
+
+constexpr int kSceneThreads = 256;
+
+template <int D>
+__global__ void __launch_bounds__(kSceneThreads)
+k_scene(const float* __restrict__ pts, long long n, float* __restrict__ part_lo, float* __restrict__ part_hi,
+        long long* __restrict__ part_bad, Scene* __restrict__ scene) {
+  float lo[D], hi[D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) { lo[k] = __int_as_float(0x7f800000); hi[k] = -__int_as_float(0x7f800000); }
+  long long bad = 0x7fffffffffffffffll;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    bool fin = true;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      float x = pts[i * D + k];
+      fin &= isfinite(x);
+      lo[k] = fminf(lo[k], x);
+      hi[k] = fmaxf(hi[k], x);
+    }
+    if (!fin && i < bad) bad = i;
+  }
+  __shared__ float s_lo[D][kSceneThreads / 32], s_hi[D][kSceneThreads / 32];
+  __shared__ long long s_bad[kSceneThreads / 32];
+  __shared__ bool s_last;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+    long long b = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = b < bad ? b : bad;
+  }
+  const int w = threadIdx.x >> 5;
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) { s_lo[k][w] = lo[k]; s_hi[k][w] = hi[k]; }
+    s_bad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int j = 1; j < kSceneThreads / 32; ++j) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) { lo[k] = fminf(lo[k], s_lo[k][j]); hi[k] = fmaxf(hi[k], s_hi[k][j]); }
+      bad = s_bad[j] < bad ? s_bad[j] : bad;
+    }
+#pragma unroll
+    for (int k = 0; k < D; ++k) { part_lo[blockIdx.x * D + k] = lo[k]; part_hi[blockIdx.x * D + k] = hi[k]; }
+    part_bad[blockIdx.x] = bad;
+    __threadfence();
+    unsigned done = atomicAdd(&scene->blocks_done, 1u);
+    s_last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last || threadIdx.x != 0) return;
+  __threadfence();
+  for (unsigned b = 0; b < gridDim.x; ++b) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      lo[k] = fminf(lo[k], __ldcg(&part_lo[b * D + k]));
+      hi[k] = fmaxf(hi[k], __ldcg(&part_hi[b * D + k]));
+    }
+    long long pb = __ldcg(&part_bad[b]);
+    bad = pb < bad ? pb : bad;
+  }
+  scene->bad_row = bad;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float l = k < D ? lo[k] : 0.f, h = k < D ? hi[k] : 0.f;
+    scene->flo[k] = l;
+    scene->fhi[k] = h;
+    double ext = __dsub_rn((double)h, (double)l);
+    scene->lo[k] = (double)l;
+    scene->inv[k] = ext > 0.0 ? __drcp_rn(ext) : 0.0;   // IEEE 1/ext (geometry.py:205)
+  }
+  scene->blocks_done = 0;
+}
+
+// Spread the low bits of v so consecutive bits land D positions apart.
+__device__ __forceinline__ unsigned long long spread_bits3(unsigned long long v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x001f00000000ffffull;
+  v = (v | (v << 16)) & 0x001f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+__device__ __forceinline__ unsigned long long spread_bits2(unsigned long long v) {
+  v &= 0x7fffffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+// Lattice cell of one coordinate (geometry.py:169-177): f64 (x - lo) * inv,
+// clamped to [0, nextafter(1, 0)], scaled by 2^bits and truncated.
+__device__ __forceinline__ unsigned long long lattice_cell(float x, double lo, double inv, double scale) {
+  double t = __dmul_rn(__dsub_rn((double)x, lo), inv);
+  const double below_one = 0x1.fffffffffffffp-1;
+  if (t < 0.0) t = 0.0;
+  else if (t > below_one) t = below_one;
+  return __double2ull_rz(__dmul_rn(t, scale));
+}
+
+template <int D>
+__global__ void k_morton(const float* __restrict__ pts, long long n, const Scene* __restrict__ scene,
+                         unsigned long long* __restrict__ codes) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (D == 3) {
+    const double scale = 2097152.0;   // 2^21
+    unsigned long long cx = lattice_cell(pts[i * 3 + 0], scene->lo[0], scene->inv[0], scale);
+    unsigned long long cy = lattice_cell(pts[i * 3 + 1], scene->lo[1], scene->inv[1], scale);
+    unsigned long long cz = lattice_cell(pts[i * 3 + 2], scene->lo[2], scene->inv[2], scale);
+    codes[i] = (spread_bits3(cx) << 2) | (spread_bits3(cy) << 1) | spread_bits3(cz);
+  } else {
+    const double scale = 2147483648.0;   // 2^31
+    unsigned long long cx = lattice_cell(pts[i * 2 + 0], scene->lo[0], scene->inv[0], scale);
+    unsigned long long cy = lattice_cell(pts[i * 2 + 1], scene->lo[1], scene->inv[1], scale);
+    codes[i] = (spread_bits2(cx) << 1) | spread_bits2(cy);
+  }
+}
+
+template <int D>
+__global__ void k_gather(const float* __restrict__ pts, long long n, const unsigned* __restrict__ perm,
+                         float4* __restrict__ spts, unsigned* __restrict__ iperm) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  unsigned p = perm[s];
+  float4 v;
+  v.x = pts[(long long)p * D + 0];
+  v.y = pts[(long long)p * D + 1];
+  v.z = D == 3 ? pts[(long long)p * D + 2] : 0.f;
+  v.w = __uint_as_float(p);
+  spts[s] = v;
+  iperm[p] = (unsigned)s;
+}
+
+// Common-prefix length of augmented keys (code, slot); -1 out of range (bvh.py:138-149).
+__device__ __forceinline__ int aug_prefix(const unsigned long long* __restrict__ c, long long n, long long i, long long j) {
+  if (j < 0 || j >= n) return -1;
+  unsigned long long a = c[i], b = c[j];
+  if (a != b) return __clzll((long long)(a ^ b));
+  return 64 + __clzll((long long)((unsigned long long)i ^ (unsigned long long)j));
+}
+
+// node ref packing: internal i -> i, leaf slot s -> ~s
+__device__ __forceinline__ int leaf_ref(long long s) { return ~(int)s; }
+
+template <class Node>
+__global__ void k_karras(const unsigned long long* __restrict__ sc, long long n, Node* __restrict__ nodes,
+                         int2* __restrict__ range, int* __restrict__ node_parent, int* __restrict__ leaf_parent) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long m = n - 1;
+  if (i >= m) return;
+  const int dir = aug_prefix(sc, n, i, i + 1) > aug_prefix(sc, n, i, i - 1) ? 1 : -1;
+  const int floor_len = aug_prefix(sc, n, i, i - dir);
+  long long span = 2;
+  while (aug_prefix(sc, n, i, i + span * dir) > floor_len) span <<= 1;
+  long long len = 0;
+  for (long long step = span >> 1; step >= 1; step >>= 1)
+    if (aug_prefix(sc, n, i, i + (len + step) * dir) > floor_len) len += step;
+  const long long j = i + len * dir;
+  const int node_len = aug_prefix(sc, n, i, j);
+  long long s = 0, step = len;
+  while (step > 1) {
+    step = (step + 1) >> 1;
+    if (aug_prefix(sc, n, i, i + (s + step) * dir) > node_len) s += step;
+  }
+  const long long gamma = i + s * dir + (dir < 0 ? -1 : 0);
+  const long long lo = i < j ? i : j, hi = i < j ? j : i;
+  int lref, rref;
+  if (lo == gamma) { lref = leaf_ref(gamma); leaf_parent[gamma] = (int)(i << 1); }
+  else { lref = (int)gamma; node_parent[gamma] = (int)(i << 1); }
+  if (hi == gamma + 1) { rref = leaf_ref(gamma + 1); leaf_parent[gamma + 1] = (int)((i << 1) | 1); }
+  else { rref = (int)(gamma + 1); node_parent[gamma + 1] = (int)((i << 1) | 1); }
+  nodes[i].ref = make_int4(lref, rref, kMixed, kMixed);
+  range[i] = make_int2((int)lo, (int)hi);
+}
+
+// --- child box slots inside a node record
+__device__ __forceinline__ void put_child_box(Node3* nodes, int node, int side, const float* lo, const float* hi) {
+  float* f = reinterpret_cast<float*>(&nodes[node]);
+  float* o = f + side * 6;
+  o[0] = lo[0]; o[1] = lo[1]; o[2] = lo[2]; o[3] = hi[0]; o[4] = hi[1]; o[5] = hi[2];
+}
+__device__ __forceinline__ void put_child_box(Node2* nodes, int node, int side, const float* lo, const float* hi) {
+  float4 v = make_float4(lo[0], lo[1], hi[0], hi[1]);
+  if (side == 0) nodes[node].a = v; else nodes[node].b = v;
+}
+// L2-coherent read of both child boxes (written by other threads of this launch)
+__device__ __forceinline__ void get_union_box(const Node3* nodes, int node, float* lo, float* hi) {
+  const float4* p = reinterpret_cast<const float4*>(&nodes[node]);
+  float4 a = __ldcg(p), b = __ldcg(p + 1), c = __ldcg(p + 2);
+  lo[0] = fminf(a.x, b.z); lo[1] = fminf(a.y, b.w); lo[2] = fminf(a.z, c.x);
+  hi[0] = fmaxf(a.w, c.y); hi[1] = fmaxf(b.x, c.z); hi[2] = fmaxf(b.y, c.w);
+}
+__device__ __forceinline__ void get_union_box(const Node2* nodes, int node, float* lo, float* hi) {
+  const float4* p = reinterpret_cast<const float4*>(&nodes[node]);
+  float4 a = __ldcg(p), b = __ldcg(p + 1);
+  lo[0] = fminf(a.x, b.x); lo[1] = fminf(a.y, b.y);
+  hi[0] = fmaxf(a.z, b.z); hi[1] = fmaxf(a.w, b.w);
+  lo[2] = hi[2] = 0.f;
+}
+
+template <class Node>
+__global__ void k_refit(const float4* __restrict__ spts, long long n, Node* nodes, const int* __restrict__ node_parent,
+                        const int* __restrict__ leaf_parent, unsigned* __restrict__ arrivals, Box3* __restrict__ root_box) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  float4 p = spts[s];
+  float lo[3] = {p.x, p.y, p.z}, hi[3] = {p.x, p.y, p.z};
+  int link = leaf_parent[s];
+  for (;;) {
+    int node = link >> 1, side = link & 1;
+    put_child_box(nodes, node, side, lo, hi);
+    __threadfence();
+    if (atomicAdd(&arrivals[node], 1u) == 0) return;   // first arrival: sibling not done yet
+    __threadfence();
+    get_union_box(nodes, node, lo, hi);
+    if (node == 0) {
+      for (int k = 0; k < 3; ++k) { root_box->lo[k] = lo[k]; root_box->hi[k] = hi[k]; }
+      return;
+    }
+    link = node_parent[node];
+  }
+}
+
+// Reference-layout export of the tree (bvh.py:39-75) for parity tests.
+template <class Node>
+__global__ void k_export_tree(const Node* __restrict__ nodes, const int* __restrict__ node_parent,
+                              const int* __restrict__ leaf_parent, long long n, const Box3* __restrict__ root_box,
+                              long long* left, long long* right, long long* parent, long long* lparent,
+                              float* box_lo, float* box_hi, int d) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long m = n - 1;
+  if (i < n) lparent[i] = m > 0 ? (long long)(leaf_parent[i] >> 1) : -1;
+  if (i >= m) return;
+  int4 r = nodes[i].ref;
+  left[i] = r.x >= 0 ? (long long)r.x : m + (long long)(~r.x);
+  right[i] = r.y >= 0 ? (long long)r.y : m + (long long)(~r.y);
+  parent[i] = i == 0 ? -1 : (long long)(node_parent[i] >> 1);
+  float lo[3], hi[3];
+  if (i == 0) {
+    for (int k = 0; k < 3; ++k) { lo[k] = root_box->lo[k]; hi[k] = root_box->hi[k]; }
+  } else {
+    int link = node_parent[i];
+    int p = link >> 1, side = link & 1;
+    const float* f = reinterpret_cast<const float*>(&nodes[p]);
+    if (sizeof(Node) == sizeof(Node3)) {
+      const float* o = f + side * 6;
+      lo[0] = o[0]; lo[1] = o[1]; lo[2] = o[2]; hi[0] = o[3]; hi[1] = o[4]; hi[2] = o[5];
+    } else {
+      const float* o = f + side * 4;
+      lo[0] = o[0]; lo[1] = o[1]; hi[0] = o[2]; hi[1] = o[3]; lo[2] = hi[2] = 0.f;
+    }
+  }
+  for (int k = 0; k < d; ++k) { box_lo[i * d + k] = lo[k]; box_hi[i * d + k] = hi[k]; }
+}
+
+}  // namespace emst

@@ -1,0 +1,110 @@
+// common.cuh -- shared types and device helpers for the B200 EMST kernels.
+//
+// Layout conventions:
+//   * slot      = position in Morton (Z) order; every per-point array is slot-indexed.
+//   * perm[s]   = original point index of slot s (u32);  iperm = inverse.
+//   * node ref  = int32: >= 0 internal node (Karras index), < 0 leaf slot ~ref.
+//   * component = dense id in [0, c) per Boruvka round; MIXED = -1.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace emst {
+
+constexpr int kMixed = -1;              // mst.py:57
+constexpr int kStackCapacity = 64;      // bvh.py:36 STACK_CAPACITY
+constexpr unsigned long long kNoBound = ~0ull;   // "+inf" for u64-bit-pattern mins
+
+// One internal node's two children, fetched by a single 64-byte node visit.
+// Leaf children carry their point as a degenerate box, so leaf distances need
+// no second fetch.  Child labels are rewritten every Boruvka round.
+struct __align__(16) Node3 {
+  float4 a;   // L.lo.x L.lo.y L.lo.z L.hi.x
+  float4 b;   // L.hi.y L.hi.z R.lo.x R.lo.y
+  float4 c;   // R.lo.z R.hi.x R.hi.y R.hi.z
+  int4 ref;   // left ref, right ref, left label, right label
+};
+struct __align__(16) Node2 {
+  float4 a;   // L.lo.x L.lo.y L.hi.x L.hi.y
+  float4 b;   // R.lo.x R.lo.y R.hi.x R.hi.y
+  int4 ref;
+};
+
+template <int D> struct NodeOf;
+template <> struct NodeOf<2> { using type = Node2; };
+template <> struct NodeOf<3> { using type = Node3; };
+
+struct Box3 { float lo[3], hi[3]; };
+
+// Per-component minimum outgoing edge, ordered by (w, u, v) with w the f64
+// bit pattern (w >= 0, so bits order like values) and uv = u << 32 | v over
+// original point indices (mst.py:62-89).  All-ones = "no edge yet".
+struct __align__(16) EdgeKey {
+  unsigned long long uv;
+  unsigned long long w;
+};
+
+__device__ __forceinline__ bool key_less(unsigned long long w, unsigned long long uv,
+                                         unsigned long long bw, unsigned long long buv) {
+  return w < bw || (w == bw && uv < buv);
+}
+
+// Lexicographic 128-bit atomic min via the sm_90+ 16-byte CAS.  Reads first and
+// only CASes while strictly smaller, so contended components rarely loop.
+__device__ __forceinline__ void atomic_min_key(EdgeKey* addr, unsigned long long w, unsigned long long uv) {
+  EdgeKey cur;
+  cur.w = __ldcg(&addr->w);
+  cur.uv = __ldcg(&addr->uv);
+  while (key_less(w, uv, cur.w, cur.uv)) {
+    EdgeKey mine;
+    mine.w = w;
+    mine.uv = uv;
+    EdgeKey old = atomicCAS(addr, cur, mine);
+    if (old.w == cur.w && old.uv == cur.uv) return;
+    cur = old;
+  }
+}
+
+// Exact reference distance: f64, axis order, correctly rounded, no FMA
+// (bvh.py:284-290; SURVEY.md hazard H1).
+template <int D>
+__device__ __forceinline__ double exact_dist(const float* q, const float* p) {
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    double dx = __dsub_rn((double)q[k], (double)p[k]);
+    s = __dadd_rn(s, __dmul_rn(dx, dx));
+  }
+  return __dsqrt_rn(s);
+}
+
+// Conservative squared lower bound from q to a box in f32, every operation
+// rounded toward -inf so it never exceeds the exact squared distance.
+template <int D>
+__device__ __forceinline__ float box_lb2(const float* q, const float* lo, const float* hi) {
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    float g = 0.f;
+    if (q[k] < lo[k]) g = __fsub_rd(lo[k], q[k]);
+    else if (q[k] > hi[k]) g = __fsub_rd(q[k], hi[k]);
+    s = __fadd_rd(s, __fmul_rd(g, g));
+  }
+  return s;
+}
+
+// f32 pruning threshold that is >= radius^2 for every radius the exact f64
+// test could still accept (relative slack 2^-20 covers f64 rounding of w).
+__device__ __forceinline__ float prune_r2(double radius) {
+  if (!(radius < 1e300)) return __int_as_float(0x7f800000);
+  double r2 = radius * radius * (1.0 + 0x1p-20);
+  return __double2float_ru(r2);
+}
+
+__device__ __forceinline__ double bits_to_radius(unsigned long long b) {
+  return b >= 0x7ff0000000000000ull ? __longlong_as_double(0x7ff0000000000000ll) : __longlong_as_double((long long)b);
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+}  // namespace emst

@@ -1,0 +1,968 @@
+// emst_b200.cu -- host orchestration and the C ABI (include/emst_b200.h).
+//
+// One context per (process, device) owns a stream, a capacity-sized device
+// workspace (reused across calls) and, for world > 1, an NCCL communicator.
+// The Boruvka loop keeps every array device-resident; the host reads back 24
+// bytes per round (new component count, edge count, error bits) to steer it.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/emst_b200.h"
+#include "boruvka.cuh"
+#include "build.cuh"
+#include "radix_sort.cuh"
+#include "scan.cuh"
+
+using namespace emst;
+
+namespace {
+
+struct Failure {
+  int code;
+  char msg[256];
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  Failure f;
+  f.code = code;
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(f.msg, sizeof(f.msg), fmt, ap);
+  va_end(ap);
+  throw f;
+}
+
+#define CK(x)                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) fail(EMST_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                __FILE__, __LINE__);                                          \
+  } while (0)
+
+#define NK(x)                                                                                   \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) fail(EMST_ERR_NCCL, "%s: %s", #x, ncclGetErrorString(r_));           \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t count) {
+    if (count <= cap) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    CK(cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    cap = count;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<long long>(1, (n + threads - 1) / threads); }
+
+}  // namespace
+
+struct emst_context {
+  int device = 0, rank = 0, world = 1, vshards = 1;
+  ncclComm_t comm = nullptr;
+  cudaStream_t stream = nullptr;
+  long long launches = 0;
+  int num_sms = 148;
+
+  // build
+  DevBuf<float> pts;
+  DevBuf<Scene> scene;
+  DevBuf<float> part_lo, part_hi;
+  DevBuf<long long> part_bad;
+  DevBuf<unsigned long long> k0, k1;
+  DevBuf<unsigned> v0, v1;
+  DevBuf<unsigned> sort_hist, sort_off, sort_status, sort_misc;
+  DevBuf<float4> spts;
+  DevBuf<unsigned> perm, iperm;
+  DevBuf<unsigned char> nodes;   // Node2 / Node3 records
+  DevBuf<int2> range;
+  DevBuf<int> node_parent, leaf_parent;
+  DevBuf<unsigned> arrivals;
+  DevBuf<Box3> root_box;
+  // rounds
+  DevBuf<int> label, bprefix;
+  DevBuf<unsigned long long> ub;
+  DevBuf<EdgeKey> best, shard_keys;
+  DevBuf<int> succ, ptr, newid, fin;
+  DevBuf<unsigned> eu, ev;
+  DevBuf<unsigned long long> ew;
+  DevBuf<unsigned long long> xw, xuv;   // multi-GPU exchange
+  DevBuf<unsigned long long> scan_scratch;
+  DevBuf<long long> counters;   // [0] evals, [1] scan total, [2] err, [3] overflow
+  DevBuf<long long> out_edges;
+  DevBuf<double> out_w;
+  long long* host_counters = nullptr;   // pinned mirror of `counters`
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  size_t nodes_stride = 0;
+  int dim = 0;
+  long long n = 0;
+  bool tree_valid = false;
+  bool sort_attr_done = false;
+};
+
+namespace {
+
+template <class K, class... A>
+void launch(emst_context* c, K kernel, unsigned grid, unsigned block, size_t smem, A... args) {
+  kernel<<<grid, block, smem, c->stream>>>(args...);
+  c->launches++;
+  CK(cudaGetLastError());
+}
+
+long long* dev_counter(emst_context* c, int i) { return c->counters.p + i; }
+
+void read_counters(emst_context* c) {
+  CK(cudaMemcpyAsync(c->host_counters, c->counters.p, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+}
+
+// ------------------------------------------------------------------- scan
+template <class L, class S>
+unsigned long long run_scan(emst_context* c, long long n, L load, S store, bool want_total) {
+  long long tiles = scan_tiles(n);
+  c->scan_scratch.ensure(tiles + 1);
+  CK(cudaMemsetAsync(c->scan_scratch.p, 0, (tiles + 1) * sizeof(unsigned long long), c->stream));
+  unsigned long long* total = reinterpret_cast<unsigned long long*>(dev_counter(c, 1));
+  launch(c, k_scan<L, S>, (unsigned)tiles, kScanThreads, 0, n, c->scan_scratch.p + 1, c->scan_scratch.p, load, store,
+         want_total ? total : (unsigned long long*)nullptr);
+  return 0;
+}
+
+// ------------------------------------------------------------------- sort
+__global__ void k_iota_u32(unsigned* a, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (unsigned)i;
+}
+
+// Stable sort of (keys, vals) by the low `bits` key bits.  `iota` means vals is
+// the identity permutation (not read; generated in the first pass).  keys_alt /
+// vals_alt are the ping-pong partners; *keys_res / *vals_res receive whichever
+// pair holds the result.
+void radix_sort(emst_context* c, long long n, int bits, unsigned long long* keys, unsigned* vals, bool iota,
+                unsigned long long* keys_alt, unsigned* vals_alt, unsigned long long** keys_res, unsigned** vals_res) {
+  const int passes = (bits + kRadixBits - 1) / kRadixBits;
+  c->sort_hist.ensure(kMaxPasses * kRadix);
+  c->sort_off.ensure(kMaxPasses * kRadix);
+  c->sort_misc.ensure(16);
+  const long long tiles = sort_tiles(n);
+  c->sort_status.ensure((size_t)tiles * kRadix);
+  CK(cudaMemsetAsync(c->sort_hist.p, 0, kMaxPasses * kRadix * sizeof(unsigned), c->stream));
+  CK(cudaMemsetAsync(c->sort_misc.p, 0, 16 * sizeof(unsigned), c->stream));
+  launch(c, k_digit_histograms, (unsigned)std::min<long long>(grid_for(n, kSortThreads), (long long)c->num_sms * 4),
+         kSortThreads, 0, (const unsigned long long*)keys, n, passes, c->sort_hist.p);
+  launch(c, k_digit_offsets, (unsigned)passes, kRadix, 0, (const unsigned*)c->sort_hist.p, n, c->sort_off.p,
+         c->sort_misc.p);
+  unsigned active = 0;
+  CK(cudaMemcpyAsync(&active, c->sort_misc.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  const size_t smem = sizeof(SortSmem);
+  if (!c->sort_attr_done) {
+    CK(cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    c->sort_attr_done = true;
+  }
+  unsigned long long *kin = keys, *kout = keys_alt;
+  unsigned *vin = vals, *vout = vals_alt;
+  int launched = 0;
+  for (int p = 0; p < passes; ++p) {
+    if (!(active & (1u << p))) continue;
+    CK(cudaMemsetAsync(c->sort_status.p, 0, (size_t)tiles * kRadix * sizeof(unsigned), c->stream));
+    if (iota)
+      launch(c, k_onesweep<true>, (unsigned)tiles, kSortThreads, smem, (const unsigned long long*)kin,
+             (const unsigned*)nullptr, kout, vout, n, p * kRadixBits, (const unsigned*)(c->sort_off.p + p * kRadix),
+             c->sort_status.p, c->sort_misc.p + 1 + launched);
+    else
+      launch(c, k_onesweep<false>, (unsigned)tiles, kSortThreads, smem, (const unsigned long long*)kin,
+             (const unsigned*)vin, kout, vout, n, p * kRadixBits, (const unsigned*)(c->sort_off.p + p * kRadix),
+             c->sort_status.p, c->sort_misc.p + 1 + launched);
+    iota = false;
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+    ++launched;
+  }
+  if (iota) launch(c, k_iota_u32, grid_for(n, 256), 256, 0, vin, n);   // every pass was the identity
+  *keys_res = kin;
+  *vals_res = vin;
+}
+
+// ------------------------------------------------------------------ build
+void ensure_build(emst_context* c, long long n, int d) {
+  const size_t node_bytes = d == 3 ? sizeof(Node3) : sizeof(Node2);
+  c->pts.ensure((size_t)n * d);
+  c->scene.ensure(1);
+  c->part_lo.ensure((size_t)c->num_sms * 8 * 3);
+  c->part_hi.ensure((size_t)c->num_sms * 8 * 3);
+  c->part_bad.ensure((size_t)c->num_sms * 8);
+  c->k0.ensure(n);
+  c->k1.ensure(n);
+  c->v0.ensure(n);
+  c->v1.ensure(n);
+  c->spts.ensure(n);
+  c->perm.ensure(n);
+  c->iperm.ensure(n);
+  c->nodes.ensure((size_t)std::max<long long>(n - 1, 1) * node_bytes);
+  c->range.ensure(std::max<long long>(n - 1, 1));
+  c->node_parent.ensure(std::max<long long>(n - 1, 1));
+  c->leaf_parent.ensure(n);
+  c->arrivals.ensure(std::max<long long>(n - 1, 1));
+  c->root_box.ensure(1);
+  c->counters.ensure(8);
+  c->nodes_stride = node_bytes;
+}
+
+// Validates and builds the hierarchy; the points must already be in c->pts
+// (or at `dev_pts`).  Returns after a sync with the scene checked.
+void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
+  ensure_build(c, n, d);
+  c->tree_valid = false;
+  c->dim = d;
+  c->n = n;
+  CK(cudaMemsetAsync(c->scene.p, 0, sizeof(Scene), c->stream));
+  unsigned sg = (unsigned)std::min<long long>(grid_for(n, kSceneThreads), (long long)c->num_sms * 8);
+  if (d == 3)
+    launch(c, k_scene<3>, sg, kSceneThreads, 0, dev_pts, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
+  else
+    launch(c, k_scene<2>, sg, kSceneThreads, 0, dev_pts, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
+  if (d == 3) launch(c, k_morton<3>, grid_for(n, 256), 256, 0, dev_pts, n, (const Scene*)c->scene.p, c->k0.p);
+  else launch(c, k_morton<2>, grid_for(n, 256), 256, 0, dev_pts, n, (const Scene*)c->scene.p, c->k0.p);
+  // the scene check needs the host anyway before anything data-dependent
+  Scene sc;
+  CK(cudaMemcpyAsync(&sc, c->scene.p, sizeof(Scene), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (sc.bad_row != 0x7fffffffffffffffll) {
+    Failure f;
+    f.code = EMST_ERR_NONFINITE;
+    snprintf(f.msg, sizeof(f.msg), "point %lld has a non-finite coordinate", sc.bad_row);
+    throw f;
+  }
+  unsigned long long* skeys;
+  unsigned* svals;
+  radix_sort(c, n, d == 3 ? 63 : 62, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &skeys, &svals);
+  // sorted codes -> k-buffer `skeys`, permutation -> `svals`
+  CK(cudaMemcpyAsync(c->perm.p, svals, n * sizeof(unsigned), cudaMemcpyDeviceToDevice, c->stream));
+  if (d == 3) launch(c, k_gather<3>, grid_for(n, 256), 256, 0, dev_pts, n, (const unsigned*)c->perm.p, c->spts.p, c->iperm.p);
+  else launch(c, k_gather<2>, grid_for(n, 256), 256, 0, dev_pts, n, (const unsigned*)c->perm.p, c->spts.p, c->iperm.p);
+  if (n > 1) {
+    const long long m = n - 1;
+    CK(cudaMemsetAsync(c->arrivals.p, 0, m * sizeof(unsigned), c->stream));
+    if (d == 3) {
+      Node3* nodes = reinterpret_cast<Node3*>(c->nodes.p);
+      launch(c, k_karras<Node3>, grid_for(m, 256), 256, 0, (const unsigned long long*)skeys, n, nodes, c->range.p,
+             c->node_parent.p, c->leaf_parent.p);
+      launch(c, k_refit<Node3>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, nodes,
+             (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p);
+    } else {
+      Node2* nodes = reinterpret_cast<Node2*>(c->nodes.p);
+      launch(c, k_karras<Node2>, grid_for(m, 256), 256, 0, (const unsigned long long*)skeys, n, nodes, c->range.p,
+             c->node_parent.p, c->leaf_parent.p);
+      launch(c, k_refit<Node2>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, nodes,
+             (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p);
+    }
+  }
+  c->tree_valid = true;
+}
+
+const float* stage_points(emst_context* c, const float* pts, long long n, int d, int flags, emst_stats* st) {
+  if (flags & EMST_POINTS_ON_DEVICE) return pts;
+  c->pts.ensure((size_t)n * d);
+  CK(cudaMemcpyAsync(c->pts.p, pts, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  if (st) st->h2d_bytes += (long long)n * d * sizeof(float);
+  return c->pts.p;
+}
+
+void check_shape(long long n, int d) {
+  if (n <= 0) fail(EMST_ERR_EMPTY, "point set is empty");
+  if (d != 2 && d != 3) fail(EMST_ERR_DIM, "points must have 2 or 3 coordinates, got %d", d);
+  if (n >= (1ll << 30)) fail(EMST_ERR_TOO_LARGE, "n = %lld exceeds the 2^30 - 1 point limit", n);
+}
+
+// ----------------------------------------------------------------- rounds
+void ensure_rounds(emst_context* c, long long n) {
+  c->label.ensure(n);
+  c->bprefix.ensure(n);
+  c->ub.ensure(n);
+  c->best.ensure(n);
+  c->succ.ensure(n);
+  c->ptr.ensure(n);
+  c->newid.ensure(n);
+  c->fin.ensure(n);
+  c->eu.ensure(n);
+  c->ev.ensure(n);
+  c->ew.ensure(n);
+  if (c->world > 1) {
+    c->xw.ensure(n);
+    c->xuv.ensure(n);
+  }
+}
+
+__global__ void k_iota_int(int* a, long long n) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = (int)i;
+}
+
+// node labels + upper bounds for the current labels (phases 1-2 of a round)
+void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds) {
+  CK(cudaEventRecord(c->ev_a, c->stream));
+  RoundScanLoad load{c->label.p, c->spts.p, c->ub.p, n, c->dim, bounds};
+  RoundScanStore store{c->bprefix.p};
+  run_scan(c, n, load, store, false);
+  CK(cudaEventRecord(c->ev_b, c->stream));
+  if (n > 1) {
+    if (c->dim == 3)
+      launch(c, k_node_labels<Node3>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node3*>(c->nodes.p),
+             (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1);
+    else
+      launch(c, k_node_labels<Node2>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node2*>(c->nodes.p),
+             (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1);
+  }
+  cudaEvent_t ev_c;
+  CK(cudaEventCreate(&ev_c));
+  CK(cudaEventRecord(ev_c, c->stream));
+  CK(cudaEventSynchronize(ev_c));
+  float a = 0.f, b = 0.f;
+  CK(cudaEventElapsedTime(&a, c->ev_a, c->ev_b));
+  CK(cudaEventElapsedTime(&b, c->ev_b, ev_c));
+  CK(cudaEventDestroy(ev_c));
+  if (ms_bounds) *ms_bounds += a;
+  if (ms_labels) *ms_labels += b;
+}
+
+template <int D, bool S, bool B>
+void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
+  if (q1 <= q0) return;
+  using Node = typename NodeOf<D>::type;
+  launch(c, k_traverse<D, S, B>, grid_for(q1 - q0, kTraverseThreads), kTraverseThreads, 0,
+         (const Node*)reinterpret_cast<Node*>(c->nodes.p), (const float4*)c->spts.p, (const unsigned*)c->perm.p,
+         (const int*)c->label.p, (const unsigned long long*)c->ub.p, out, q0, q1, (const Box3*)c->root_box.p,
+         reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), reinterpret_cast<int*>(dev_counter(c, 3)));
+}
+
+void traverse_dispatch(emst_context* c, int flags, EdgeKey* out, long long q0, long long q1) {
+  const bool S = flags & EMST_SUBTREE_SKIP, B = flags & EMST_UPPER_BOUNDS;
+  if (c->dim == 3) {
+    if (S && B) traverse_range<3, true, true>(c, out, q0, q1);
+    else if (S) traverse_range<3, true, false>(c, out, q0, q1);
+    else if (B) traverse_range<3, false, true>(c, out, q0, q1);
+    else traverse_range<3, false, false>(c, out, q0, q1);
+  } else {
+    if (S && B) traverse_range<2, true, true>(c, out, q0, q1);
+    else if (S) traverse_range<2, true, false>(c, out, q0, q1);
+    else if (B) traverse_range<2, false, true>(c, out, q0, q1);
+    else traverse_range<2, false, false>(c, out, q0, q1);
+  }
+}
+
+// Phase 3: per-component minimum outgoing edge into c->best[0, comps).
+void round_find(emst_context* c, long long n, long long comps, int flags) {
+  if (c->vshards > 1) {
+    const int V = c->vshards;
+    c->shard_keys.ensure((size_t)V * comps);
+    CK(cudaMemsetAsync(c->shard_keys.p, 0xff, (size_t)V * comps * sizeof(EdgeKey), c->stream));
+    for (int g = 0; g < V; ++g) traverse_dispatch(c, flags, c->shard_keys.p + (size_t)g * comps, g * n / V, (g + 1) * n / V);
+    launch(c, k_virtual_reduce, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->shard_keys.p, V, comps, c->best.p);
+    return;
+  }
+  const long long q0 = c->rank * n / c->world, q1 = (c->rank + 1) * n / c->world;
+  traverse_dispatch(c, flags, c->best.p, q0, q1);
+  if (c->world > 1) {
+    launch(c, k_split_keys, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, c->xw.p);
+    NK(ncclAllReduce(c->xw.p, c->xw.p, comps, ncclUint64, ncclMin, c->comm, c->stream));
+    launch(c, k_mask_uv, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, (const unsigned long long*)c->xw.p,
+           comps, c->xuv.p);
+    NK(ncclAllReduce(c->xuv.p, c->xuv.p, comps, ncclUint64, ncclMin, c->comm, c->stream));
+    launch(c, k_join_keys, grid_for(comps, 256), 256, 0, c->best.p, (const unsigned long long*)c->xw.p,
+           (const unsigned long long*)c->xuv.p, comps);
+  }
+}
+
+// Phase 4: collapse the successor graph; appends edges at `edge_base`, relabels.
+// Returns the new component count (and the edges emitted via *emitted).
+long long round_merge(emst_context* c, long long n, long long comps, long long edge_base, long long* emitted) {
+  int* err = reinterpret_cast<int*>(dev_counter(c, 2));
+  launch(c, k_merge_succ, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, (const int*)c->label.p,
+         (const unsigned*)c->iperm.p, c->succ.p, err);
+  launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
+  launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, err);
+  MergeScanLoad load{c->succ.p, c->ptr.p};
+  MergeScanStore store{c->succ.p, c->ptr.p, c->best.p, c->eu.p, c->ev.p, c->ew.p, edge_base, c->newid.p};
+  run_scan(c, comps, load, store, true);
+  launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->ptr.p, (const int*)c->newid.p, comps, c->fin.p);
+  launch(c, k_relabel, grid_for(n, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
+  read_counters(c);
+  long long* h = c->host_counters;
+  if (h[2] & kErrNoEdge) fail(EMST_ERR_NO_EDGE, "a component found no valid outgoing edge");
+  if (h[2] & kErrChain) fail(EMST_ERR_CHAIN, "component chain did not terminate in a pair");
+  unsigned long long tot = (unsigned long long)h[1];
+  *emitted = (long long)(tot & 0x7fffffffull);
+  return (long long)(tot >> 31);
+}
+
+void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* w_dst) {
+  if (ne <= 0) return;
+  launch(c, k_edge_uv_keys, grid_for(ne, 256), 256, 0, (const unsigned*)c->eu.p, (const unsigned*)c->ev.p, ne, c->k0.p);
+  unsigned long long* keys;
+  unsigned* order;
+  radix_sort(c, ne, 64, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
+  // second (stable) key: the weight bits, carried in the order of the first sort
+  unsigned long long* kin = keys == c->k0.p ? c->k1.p : c->k0.p;
+  unsigned* vin_alt = order == c->v1.p ? c->v0.p : c->v1.p;
+  launch(c, k_edge_w_keys, grid_for(ne, 256), 256, 0, (const unsigned long long*)c->ew.p, (const unsigned*)order, ne, kin);
+  unsigned long long* keys2;
+  unsigned* order2;
+  radix_sort(c, ne, 64, kin, order, false, keys, vin_alt, &keys2, &order2);
+  launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, (const unsigned*)c->eu.p, (const unsigned*)c->ev.p,
+         (const unsigned long long*)c->ew.p, (const unsigned*)order2, ne, edges_dst, w_dst);
+}
+
+int max_iterations(long long n) {
+  if (n <= 1) return 0;
+  int k = 0;
+  while ((1ll << k) < n) ++k;
+  return std::max(k, 1);
+}
+
+// The full solve: build, rounds, final order.  Outputs land in device buffers
+// c->out_edges / c->out_w unless the caller's device pointers are given.
+void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags, long long* edges_dev,
+           double* w_dev, emst_stats* st) {
+  cudaEvent_t t0, t1, t2, t3;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
+  CK(cudaEventCreate(&t2));
+  CK(cudaEventCreate(&t3));
+  CK(cudaEventRecord(t0, c->stream));
+  build_tree(c, dev_pts, n, d);
+  CK(cudaEventRecord(t1, c->stream));
+  ensure_rounds(c, n);
+  CK(cudaMemsetAsync(c->counters.p, 0, 8 * sizeof(long long), c->stream));
+  launch(c, k_iota_int, grid_for(n, 256), 256, 0, c->label.p, n);
+  long long comps = n, edges = 0;
+  const int max_it = max_iterations(n);
+  st->component_counts[0] = n;
+  st->num_counts = 1;
+  double ms_labels = 0, ms_bounds = 0, ms_find = 0, ms_merge = 0;
+  const bool bounds = flags & EMST_UPPER_BOUNDS;
+  while (comps > 1) {
+    st->iterations++;
+    if (st->iterations > max_it) fail(EMST_ERR_ITER, "exceeded the %d-iteration bound for n=%lld", max_it, n);
+    CK(cudaMemsetAsync(c->ub.p, 0xff, comps * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->best.p, 0xff, comps * sizeof(EdgeKey), c->stream));
+    round_prepare(c, n, bounds, &ms_labels, &ms_bounds);
+    CK(cudaEventRecord(c->ev_a, c->stream));
+    round_find(c, n, comps, flags);
+    CK(cudaEventRecord(c->ev_b, c->stream));
+    long long emitted = 0;
+    long long next = round_merge(c, n, comps, edges, &emitted);
+    float a = 0.f;
+    CK(cudaEventElapsedTime(&a, c->ev_a, c->ev_b));
+    ms_find += a;
+    CK(cudaEventRecord(c->ev_a, c->stream));
+    CK(cudaEventSynchronize(c->ev_a));
+    CK(cudaEventElapsedTime(&a, c->ev_b, c->ev_a));
+    ms_merge += a;
+    if (c->host_counters[3]) fail(EMST_ERR_STACK, "edge traversal exceeded %d stacked nodes", kStackCapacity);
+    if (next >= comps) fail(EMST_ERR_NO_REDUCE, "merge did not reduce the component count");
+    edges += emitted;
+    comps = next;
+    if (st->num_counts < 64) st->component_counts[st->num_counts++] = comps;
+  }
+  if (edges != n - 1) fail(EMST_ERR_COUNT, "collected %lld edges for %lld points", edges, n);
+  sort_and_emit(c, edges, edges_dev, w_dev);
+  CK(cudaEventRecord(t2, c->stream));
+  CK(cudaEventSynchronize(t2));
+  read_counters(c);
+  long long evals = c->host_counters[0];
+  if (c->world > 1) {
+    // total work counter over ranks (instrumentation only)
+    NK(ncclAllReduce(dev_counter(c, 0), dev_counter(c, 0), 1, ncclInt64, ncclSum, c->comm, c->stream));
+    read_counters(c);
+    evals = c->host_counters[0];
+  }
+  st->leaf_distance_evals = evals;
+  float ms_tree = 0, ms_mst = 0;
+  CK(cudaEventElapsedTime(&ms_tree, t0, t1));
+  CK(cudaEventElapsedTime(&ms_mst, t1, t2));
+  st->phase_ms[EMST_PHASE_TREE] = ms_tree;
+  st->phase_ms[EMST_PHASE_CORE] = 0.0;
+  st->phase_ms[EMST_PHASE_REDUCE_LABELS] = ms_labels;
+  st->phase_ms[EMST_PHASE_UPPER_BOUNDS] = ms_bounds;
+  st->phase_ms[EMST_PHASE_FIND_EDGES] = ms_find;
+  st->phase_ms[EMST_PHASE_MERGE] = ms_merge;
+  st->phase_ms[EMST_PHASE_MST] = ms_mst;
+  st->phase_ms[EMST_PHASE_TOTAL] = ms_tree + ms_mst;
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  cudaEventDestroy(t2);
+  cudaEventDestroy(t3);
+}
+
+int finish(const Failure& f, char* err, size_t errlen) {
+  if (err && errlen) snprintf(err, errlen, "%s", f.msg);
+  return f.code;
+}
+
+void set_device(emst_context* c) { CK(cudaSetDevice(c->device)); }
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* emst_build_info(void) { return "emst_b200 sm_100a onesweep-lbvh-boruvka v1"; }
+
+int emst_nccl_unique_id(void* id_out_128, char* err, size_t errlen) {
+  try {
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL id size");
+    memcpy(id_out_128, &id, sizeof(id));
+    return EMST_OK;
+  } catch (const Failure& f) {
+    return finish(f, err, errlen);
+  }
+}
+
+int emst_context_create(int device, int rank, int world, const void* nccl_id, emst_context** out, char* err,
+                        size_t errlen) {
+  emst_context* c = nullptr;
+  try {
+    if (world < 1 || rank < 0 || rank >= world) fail(EMST_ERR_PARAM, "bad rank %d / world %d", rank, world);
+    c = new emst_context();
+    c->device = device;
+    c->rank = rank;
+    c->world = world;
+    set_device(c);
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaMallocHost(&c->host_counters, 8 * sizeof(long long)));
+    CK(cudaEventCreate(&c->ev_a));
+    CK(cudaEventCreate(&c->ev_b));
+    c->counters.ensure(8);
+    if (world > 1) {
+      if (!nccl_id) fail(EMST_ERR_PARAM, "world > 1 needs an NCCL unique id");
+      ncclUniqueId id;
+      memcpy(&id, nccl_id, sizeof(id));
+      NK(ncclCommInitRank(&c->comm, world, id, rank));
+    }
+    *out = c;
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) emst_context_destroy(c);
+    return finish(f, err, errlen);
+  }
+}
+
+int emst_context_destroy(emst_context* c) {
+  if (!c) return EMST_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->comm) ncclCommDestroy(c->comm);
+  c->pts.release(); c->scene.release(); c->part_lo.release(); c->part_hi.release(); c->part_bad.release();
+  c->k0.release(); c->k1.release(); c->v0.release(); c->v1.release();
+  c->sort_hist.release(); c->sort_off.release(); c->sort_status.release(); c->sort_misc.release();
+  c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
+  c->node_parent.release(); c->leaf_parent.release(); c->arrivals.release(); c->root_box.release();
+  c->label.release(); c->bprefix.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
+  c->succ.release(); c->ptr.release(); c->newid.release(); c->fin.release();
+  c->eu.release(); c->ev.release(); c->ew.release(); c->xw.release(); c->xuv.release();
+  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release();
+  if (c->host_counters) cudaFreeHost(c->host_counters);
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_b) cudaEventDestroy(c->ev_b);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return EMST_OK;
+}
+
+int emst_context_set_virtual_shards(emst_context* c, int shards) {
+  if (!c || shards < 1 || shards > 64) return EMST_ERR_PARAM;
+  c->vshards = shards;
+  return EMST_OK;
+}
+
+int emst_boruvka(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t* edges_out,
+                 double* weights_out, emst_stats* stats, char* err, size_t errlen) {
+  emst_stats local;
+  emst_stats* st = stats ? stats : &local;
+  memset(st, 0, sizeof(*st));
+  st->world = c ? c->world : 1;
+  st->rank = c ? c->rank : 0;
+  try {
+    if (!c) fail(EMST_ERR_PARAM, "null context");
+    set_device(c);
+    check_shape(n, d);
+    const long long launches0 = c->launches;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, c->stream));
+    const float* dp = stage_points(c, pts, n, d, flags, st);
+    const long long ne = n - 1;
+    long long* edst;
+    double* wdst;
+    if (flags & EMST_OUTPUT_ON_DEVICE) {
+      edst = reinterpret_cast<long long*>(edges_out);
+      wdst = weights_out;
+    } else {
+      c->out_edges.ensure(2 * std::max<long long>(ne, 1));
+      c->out_w.ensure(std::max<long long>(ne, 1));
+      edst = c->out_edges.p;
+      wdst = c->out_w.p;
+    }
+    if (n == 1) {
+      // a single point has an empty tree and no iterations (mst.py:671)
+      ensure_build(c, n, d);
+      CK(cudaMemsetAsync(c->scene.p, 0, sizeof(Scene), c->stream));
+      if (d == 3) launch(c, k_scene<3>, 1, kSceneThreads, 0, dp, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
+      else launch(c, k_scene<2>, 1, kSceneThreads, 0, dp, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
+      Scene sc;
+      CK(cudaMemcpyAsync(&sc, c->scene.p, sizeof(Scene), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+      if (sc.bad_row != 0x7fffffffffffffffll) fail(EMST_ERR_NONFINITE, "point %lld has a non-finite coordinate", sc.bad_row);
+      st->component_counts[0] = 1;
+      st->num_counts = 1;
+    } else {
+      solve(c, dp, n, d, flags, edst, wdst, st);
+      if (!(flags & EMST_OUTPUT_ON_DEVICE)) {
+        CK(cudaMemcpyAsync(edges_out, edst, 2 * ne * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(weights_out, wdst, ne * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        st->d2h_bytes += ne * (2 * sizeof(long long) + sizeof(double));
+      }
+    }
+    CK(cudaEventRecord(e1, c->stream));
+    CK(cudaEventSynchronize(e1));
+    float total = 0.f;
+    CK(cudaEventElapsedTime(&total, e0, e1));
+    st->phase_ms[EMST_PHASE_TOTAL] = total;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    st->kernel_launches = c->launches - launches0;
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (f.code == EMST_ERR_NONFINITE) {
+      long long row = -1;
+      sscanf(f.msg, "point %lld", &row);
+      st->bad_row = row;
+    }
+    if (c) cudaStreamSynchronize(c->stream);
+    return finish(f, err, errlen);
+  }
+}
+
+int emst_morton_codes(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, uint64_t* codes_out,
+                      char* err, size_t errlen) {
+  try {
+    set_device(c);
+    check_shape(n, d);
+    const float* dp = stage_points(c, pts, n, d, flags, nullptr);
+    ensure_build(c, n, d);
+    CK(cudaMemsetAsync(c->scene.p, 0, sizeof(Scene), c->stream));
+    unsigned sg = (unsigned)std::min<long long>(grid_for(n, kSceneThreads), (long long)c->num_sms * 8);
+    if (d == 3) {
+      launch(c, k_scene<3>, sg, kSceneThreads, 0, dp, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
+      launch(c, k_morton<3>, grid_for(n, 256), 256, 0, dp, n, (const Scene*)c->scene.p, c->k0.p);
+    } else {
+      launch(c, k_scene<2>, sg, kSceneThreads, 0, dp, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
+      launch(c, k_morton<2>, grid_for(n, 256), 256, 0, dp, n, (const Scene*)c->scene.p, c->k0.p);
+    }
+    CK(cudaMemcpyAsync(codes_out, c->k0.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) cudaStreamSynchronize(c->stream);
+    return finish(f, err, errlen);
+  }
+}
+
+int emst_build(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t* perm, int64_t* left,
+               int64_t* right, int64_t* parent, int64_t* leaf_parent, float* box_lo, float* box_hi, char* err,
+               size_t errlen) {
+  try {
+    set_device(c);
+    check_shape(n, d);
+    const float* dp = stage_points(c, pts, n, d, flags, nullptr);
+    build_tree(c, dp, n, d);
+    const long long m = n - 1;
+    // export in the reference's int64 layout through scratch device buffers
+    DevBuf<long long> tmp;
+    tmp.ensure((size_t)(4 * std::max<long long>(m, 1) + n));
+    DevBuf<float> boxes;
+    boxes.ensure((size_t)2 * std::max<long long>(m, 1) * d);
+    long long *dl = tmp.p, *dr = dl + std::max<long long>(m, 1), *dpar = dr + std::max<long long>(m, 1),
+              *dlp = dpar + std::max<long long>(m, 1);
+    if (d == 3)
+      launch(c, k_export_tree<Node3>, grid_for(n, 256), 256, 0, (const Node3*)reinterpret_cast<Node3*>(c->nodes.p),
+             (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, n, (const Box3*)c->root_box.p, dl, dr, dpar,
+             dlp, boxes.p, boxes.p + std::max<long long>(m, 1) * d, d);
+    else
+      launch(c, k_export_tree<Node2>, grid_for(n, 256), 256, 0, (const Node2*)reinterpret_cast<Node2*>(c->nodes.p),
+             (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, n, (const Box3*)c->root_box.p, dl, dr, dpar,
+             dlp, boxes.p, boxes.p + std::max<long long>(m, 1) * d, d);
+    std::vector<unsigned> hperm(n);
+    CK(cudaMemcpyAsync(hperm.data(), c->perm.p, n * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+    if (m > 0) {
+      CK(cudaMemcpyAsync(left, dl, m * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(right, dr, m * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(parent, dpar, m * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(box_lo, boxes.p, m * d * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(box_hi, boxes.p + std::max<long long>(m, 1) * d, m * d * sizeof(float),
+                         cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaMemcpyAsync(leaf_parent, dlp, n * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (long long i = 0; i < n; ++i) perm[i] = hperm[i];
+    if (n == 1) leaf_parent[0] = -1;
+    tmp.release();
+    boxes.release();
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) cudaStreamSynchronize(c->stream);
+    return finish(f, err, errlen);
+  }
+}
+
+}  // extern "C"
+
+// ---------------------------------------------- per-round building blocks
+// These operate on reference-layout state: labels are representative point
+// indices (any value < n works as an identifier), per-component arrays are
+// n-sized and indexed by label.  Slot-space labels are gathered through perm.
+
+namespace {
+
+__global__ void k_labels_to_slots(const long long* __restrict__ labels_pt, const unsigned* __restrict__ perm, long long n,
+                                  int* __restrict__ label_slot) {
+  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s < n) label_slot[s] = (int)labels_pt[perm[s]];
+}
+
+template <class Node>
+__global__ void k_export_node_labels(const Node* __restrict__ nodes, long long m, const long long* __restrict__ labels_pt,
+                                     const unsigned* __restrict__ perm, const int* __restrict__ node_parent,
+                                     const int* __restrict__ label_slot, const int2* __restrict__ range,
+                                     const int* __restrict__ bprefix, long long* __restrict__ il) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  // node i's own label is held in its parent's record; the root's is derived directly
+  if (i == 0) {
+    int2 r = range[0];
+    il[0] = bprefix[r.y] == bprefix[r.x] ? (long long)label_slot[r.x] : (long long)kMixed;
+    return;
+  }
+  int link = node_parent[i];
+  int4 ref = nodes[link >> 1].ref;
+  il[i] = (link & 1) ? ref.w : ref.z;
+}
+
+void prepare_labels_from_host(emst_context* c, const int64_t* labels, long long n) {
+  ensure_rounds(c, n);
+  DevBuf<long long> lab;
+  lab.ensure(n);
+  CK(cudaMemcpyAsync(lab.p, labels, n * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+  launch(c, k_labels_to_slots, grid_for(n, 256), 256, 0, (const long long*)lab.p, (const unsigned*)c->perm.p, n, c->label.p);
+  CK(cudaStreamSynchronize(c->stream));
+  lab.release();
+}
+
+}  // namespace
+
+extern "C" {
+
+int emst_reduce_labels(emst_context* c, const float* pts, int64_t n, int32_t d, const int64_t* labels,
+                       int64_t* internal_labels, char* err, size_t errlen) {
+  try {
+    set_device(c);
+    check_shape(n, d);
+    const float* dp = stage_points(c, pts, n, d, 0, nullptr);
+    build_tree(c, dp, n, d);
+    if (n == 1) return EMST_OK;
+    prepare_labels_from_host(c, labels, n);
+    round_prepare(c, n, false, nullptr, nullptr);
+    DevBuf<long long> il;
+    il.ensure(n - 1);
+    if (d == 3)
+      launch(c, k_export_node_labels<Node3>, grid_for(n - 1, 256), 256, 0, (const Node3*)reinterpret_cast<Node3*>(c->nodes.p),
+             n - 1, (const long long*)nullptr, (const unsigned*)c->perm.p, (const int*)c->node_parent.p,
+             (const int*)c->label.p, (const int2*)c->range.p, (const int*)c->bprefix.p, il.p);
+    else
+      launch(c, k_export_node_labels<Node2>, grid_for(n - 1, 256), 256, 0, (const Node2*)reinterpret_cast<Node2*>(c->nodes.p),
+             n - 1, (const long long*)nullptr, (const unsigned*)c->perm.p, (const int*)c->node_parent.p,
+             (const int*)c->label.p, (const int2*)c->range.p, (const int*)c->bprefix.p, il.p);
+    CK(cudaMemcpyAsync(internal_labels, il.p, (n - 1) * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    il.release();
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) cudaStreamSynchronize(c->stream);
+    return finish(f, err, errlen);
+  }
+}
+
+int emst_compute_upper_bounds(emst_context* c, const float* pts, int64_t n, int32_t d, const int64_t* labels,
+                              double* ub_out, char* err, size_t errlen) {
+  try {
+    set_device(c);
+    check_shape(n, d);
+    const float* dp = stage_points(c, pts, n, d, 0, nullptr);
+    build_tree(c, dp, n, d);
+    prepare_labels_from_host(c, labels, n);
+    CK(cudaMemsetAsync(c->ub.p, 0xff, n * sizeof(unsigned long long), c->stream));
+    round_prepare(c, n, true, nullptr, nullptr);
+    std::vector<unsigned long long> bits(n);
+    CK(cudaMemcpyAsync(bits.data(), c->ub.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (long long i = 0; i < n; ++i) {
+      unsigned long long b = bits[i] >= 0x7ff0000000000000ull ? 0x7ff0000000000000ull : bits[i];
+      memcpy(&ub_out[i], &b, 8);
+    }
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) cudaStreamSynchronize(c->stream);
+    return finish(f, err, errlen);
+  }
+}
+
+int emst_find_component_outgoing_edges(emst_context* c, const float* pts, int64_t n, int32_t d, const int64_t* labels,
+                                       const double* ub, int32_t flags, int64_t* best_u, int64_t* best_v,
+                                       double* best_w, int64_t* leaf_evals, char* err, size_t errlen) {
+  try {
+    set_device(c);
+    check_shape(n, d);
+    if (n < 2) fail(EMST_ERR_NOTHING, "a single component has no outgoing edges");
+    const float* dp = stage_points(c, pts, n, d, 0, nullptr);
+    build_tree(c, dp, n, d);
+    prepare_labels_from_host(c, labels, n);
+    std::vector<unsigned long long> bits(n);
+    for (long long i = 0; i < n; ++i) {
+      double w = (flags & EMST_UPPER_BOUNDS) ? ub[i] : __builtin_inf();
+      memcpy(&bits[i], &w, 8);
+      if (!(w >= 0.0) || w == __builtin_inf()) bits[i] = ~0ull;
+    }
+    CK(cudaMemcpyAsync(c->ub.p, bits.data(), n * sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
+    // node labels only (bounds are caller-provided)
+    round_prepare(c, n, false, nullptr, nullptr);
+    CK(cudaMemsetAsync(c->best.p, 0xff, n * sizeof(EdgeKey), c->stream));
+    CK(cudaMemsetAsync(c->counters.p, 0, 8 * sizeof(long long), c->stream));
+    round_find(c, n, n, flags);
+    std::vector<EdgeKey> keys(n);
+    CK(cudaMemcpyAsync(keys.data(), c->best.p, n * sizeof(EdgeKey), cudaMemcpyDeviceToHost, c->stream));
+    read_counters(c);
+    if (c->host_counters[3]) fail(EMST_ERR_STACK, "edge traversal exceeded %d stacked nodes", kStackCapacity);
+    for (long long i = 0; i < n; ++i) {
+      if (keys[i].uv == ~0ull) {
+        best_u[i] = -1;
+        best_v[i] = -1;
+        best_w[i] = __builtin_inf();
+      } else {
+        best_u[i] = (long long)(keys[i].uv >> 32);
+        best_v[i] = (long long)(keys[i].uv & 0xffffffffull);
+        memcpy(&best_w[i], &keys[i].w, 8);
+      }
+    }
+    if (leaf_evals) *leaf_evals = c->host_counters[0];
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) cudaStreamSynchronize(c->stream);
+    return finish(f, err, errlen);
+  }
+}
+
+}  // extern "C"
+
+namespace {
+__global__ void k_cluster_min(const int* __restrict__ ptr, const long long* __restrict__ reps, long long s,
+                              long long* __restrict__ cmin) {
+  long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k < s) atomicMin(&cmin[ptr[k]], reps[k]);
+}
+}  // namespace
+
+extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* reps, int64_t s, const int64_t* best_u,
+                                     const int64_t* best_v, const double* best_w, int64_t* labels, int64_t* out_u,
+                                     int64_t* out_v, double* out_w, int64_t* n_edges, int64_t* new_reps,
+                                     int64_t* n_new, char* err, size_t errlen) {
+  // Dense-id formulation of mst.py:517-547: component k <-> reps[k].
+  try {
+    set_device(c);
+    if (s < 1 || n < 1) fail(EMST_ERR_PARAM, "empty merge");
+    ensure_rounds(c, n);
+    c->iperm.ensure(n);
+    c->counters.ensure(8);
+    std::vector<int> dense(n, -1), lab(n);
+    for (long long k = 0; k < s; ++k) dense[reps[k]] = (int)k;
+    for (long long i = 0; i < n; ++i) lab[i] = dense[labels[i]];
+    std::vector<EdgeKey> keys(s);
+    for (long long k = 0; k < s; ++k) {
+      long long r = reps[k];
+      if (best_v[r] < 0) { keys[k].uv = ~0ull; keys[k].w = ~0ull; continue; }
+      keys[k].uv = ((unsigned long long)best_u[r] << 32) | (unsigned long long)best_v[r];
+      memcpy(&keys[k].w, &best_w[r], 8);
+    }
+    std::vector<unsigned> ident(n);
+    for (long long i = 0; i < n; ++i) ident[i] = (unsigned)i;   // point order == "slot" order here
+    CK(cudaMemcpyAsync(c->label.p, lab.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->iperm.p, ident.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->best.p, keys.data(), s * sizeof(EdgeKey), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->counters.p, 0, 8 * sizeof(long long), c->stream));
+    long long emitted = 0;
+    long long next = round_merge(c, n, s, 0, &emitted);
+    if (next >= s) fail(EMST_ERR_NO_REDUCE, "merge did not reduce the component count");
+    // reference labels: each cluster adopts its smallest representative
+    DevBuf<long long> dreps, cmin;
+    dreps.ensure(s);
+    cmin.ensure(s);
+    CK(cudaMemcpyAsync(dreps.p, reps, s * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(cmin.p, 0x7f, s * sizeof(long long), c->stream));
+    launch(c, k_cluster_min, grid_for(s, 256), 256, 0, (const int*)c->ptr.p, (const long long*)dreps.p, s, cmin.p);
+    std::vector<int> ptr(s), newlab(n);
+    std::vector<long long> cm(s);
+    std::vector<unsigned> eu(emitted), ev(emitted);
+    std::vector<unsigned long long> ew(emitted);
+    CK(cudaMemcpyAsync(ptr.data(), c->ptr.p, s * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(cm.data(), cmin.p, s * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+    if (emitted) {
+      CK(cudaMemcpyAsync(eu.data(), c->eu.p, emitted * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(ev.data(), c->ev.p, emitted * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(ew.data(), c->ew.p, emitted * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    for (long long i = 0; i < n; ++i) {
+      int k = lab[i];
+      labels[i] = k >= 0 ? cm[ptr[k]] : labels[i];
+    }
+    long long nn = 0;
+    for (long long k = 0; k < s; ++k)
+      if (ptr[k] == (int)k) new_reps[nn++] = cm[k];
+    std::sort(new_reps, new_reps + nn);
+    for (long long e = 0; e < emitted; ++e) {
+      out_u[e] = eu[e];
+      out_v[e] = ev[e];
+      memcpy(&out_w[e], &ew[e], 8);
+    }
+    *n_edges = emitted;
+    *n_new = nn;
+    dreps.release();
+    cmin.release();
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) cudaStreamSynchronize(c->stream);
+    return finish(f, err, errlen);
+  }
+}

@@ -1,0 +1,324 @@
+"""The drop-in entry point: ``boruvka_emst`` on a B200 (pkg/src/emst/mst.py:578-769).
+
+Same signature, validation order, exceptions and ``MstResult`` as the
+reference.  The work happens in ``libemst_b200.so``: every phase of the
+single-tree Boruvka loop is a hand-written sm_100a kernel;
+this module only validates arguments, hands the points over (host numpy array
+or a CUDA float32 tensor, zero-copy) and wraps the outputs.
+
+The per-round building blocks (``reduce_labels``, ``compute_upper_bounds``,
+``find_component_outgoing_edges``, ``merge_components``; mst.py:436-547) are
+exported too, each backed by the same GPU kernels the loop uses.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .bvh import Bvh, _device_points
+from .errors import (
+    DimensionMismatchError,
+    InternalInvariantViolation,
+    InvalidParameterError,
+    NoOutgoingEdgeError,
+    NothingToFindError,
+)
+from .geometry import as_point_array
+
+MIXED = -1   # mst.py:57
+
+
+@dataclass(frozen=True)
+class WeightedEdge:
+    """Undirected edge with canonical u < v, ordered by (weight, u, v) (mst.py:62-89)."""
+
+    u: int
+    v: int
+    weight: float
+
+    def __post_init__(self):
+        if self.u == self.v:
+            raise InvalidParameterError(f"self edge at {self.u}")
+        if self.u < 0 or self.v < 0:
+            raise InvalidParameterError("edge endpoints must be non-negative")
+        if self.u > self.v:
+            lo, hi = self.v, self.u
+            object.__setattr__(self, "u", lo)
+            object.__setattr__(self, "v", hi)
+
+    @property
+    def key(self) -> tuple[float, int, int]:
+        return (self.weight, self.u, self.v)
+
+    def __lt__(self, other: "WeightedEdge") -> bool:
+        return self.key < other.key
+
+
+@dataclass
+class ComponentState:
+    """Per-point representative labels, internal-node labels and radii (mst.py:92-117)."""
+
+    labels: np.ndarray
+    internal_labels: np.ndarray
+    upper_bounds: np.ndarray
+
+    @classmethod
+    def initial(cls, bvh: Bvh) -> "ComponentState":
+        n = bvh.num_points
+        return cls(np.arange(n, dtype=np.int64), np.full(max(n - 1, 0), MIXED, dtype=np.int64),
+                   np.full(n, np.inf, dtype=np.float64))
+
+    @property
+    def num_components(self) -> int:
+        return int(np.unique(self.labels).shape[0])
+
+
+@dataclass
+class OutgoingEdges:
+    """Cheapest outgoing edge per live component; u, v, w indexed by representative (mst.py:120-137)."""
+
+    reps: np.ndarray
+    u: np.ndarray
+    v: np.ndarray
+    w: np.ndarray
+    leaf_distance_evals: int
+
+    def edge(self, rep: int) -> WeightedEdge:
+        if self.v[rep] < 0:
+            raise NoOutgoingEdgeError(f"component {rep} has no recorded edge")
+        return WeightedEdge(int(self.u[rep]), int(self.v[rep]), float(self.w[rep]))
+
+
+@dataclass
+class MergeOutcome:
+    """One iteration's collapse of the component graph (mst.py:140-155)."""
+
+    num_components: int
+    edge_u: np.ndarray
+    edge_v: np.ndarray
+    edge_w: np.ndarray
+    new_reps: np.ndarray
+
+    @property
+    def edges(self) -> list[WeightedEdge]:
+        return [WeightedEdge(int(u), int(v), float(w)) for u, v, w in zip(self.edge_u, self.edge_v, self.edge_w)]
+
+
+@dataclass
+class MstResult:
+    """A spanning tree plus run instrumentation (mst.py:158-182).
+
+    edges (n-1, 2) int64 with u < v, rows sorted by (weight, u, v); weights
+    aligned float64; phase_timings in seconds (device-timed phases, host-timed
+    total); component_counts from n down to 1.
+    """
+
+    edges: np.ndarray
+    weights: np.ndarray
+    total_weight: float
+    iterations: int
+    phase_timings: dict = field(default_factory=dict)
+    component_counts: list = field(default_factory=list)
+    leaf_distance_evals: int = 0
+    threads: int = 1
+    kernel_launches: int = 0
+    gpus: int = 1
+
+    def edge_list(self) -> list[WeightedEdge]:
+        return [WeightedEdge(int(u), int(v), float(w)) for (u, v), w in zip(self.edges, self.weights)]
+
+
+def _resolve_threads(threads) -> int:
+    """Validated like mst.py:550-559; the GPU build reports one host thread."""
+    if not isinstance(threads, (int, np.integer)):
+        raise InvalidParameterError(f"threads must be an integer, got {threads!r}")
+    if int(threads) < 0:
+        raise InvalidParameterError(f"threads must be >= 0, got {int(threads)}")
+    return 1
+
+
+def _resolve_metric(metric) -> str:
+    """mst.py:562-575; only the Euclidean metric is built for the GPU (SURVEY.md §8f row 1 is next)."""
+    if isinstance(metric, str):
+        name = metric.strip().lower().replace("_", "-")
+        if name == "euclidean":
+            return "euclidean"
+        if name in ("mrd", "mutual-reachability"):
+            return "mrd"
+        raise InvalidParameterError(f"metric must be 'euclidean' or 'mrd', got {metric!r}")
+    if type(metric).__name__ == "Euclidean":
+        return "euclidean"
+    if type(metric).__name__ == "MutualReachability":
+        return "mrd"
+    raise InvalidParameterError(f"unknown metric {metric!r}")
+
+
+def boruvka_emst(points, metric="euclidean", k_pts: int = 1, *, threads: int = 0, subtree_skip: bool = True,
+                 upper_bound_seeding: bool = True, context: _lib.Context | None = None) -> MstResult:
+    """Euclidean minimum spanning tree of (n, d) points, d in {2, 3}, on the GPU.
+
+    Drop-in for the reference's ``boruvka_emst`` (mst.py:578-624): identical
+    edges and weights (bit for bit, including ties), iterations and
+    component_counts.  ``points`` may be array-like (copied host -> device) or a
+    CUDA float32 tensor (used in place).  ``context`` selects a device / NCCL
+    rank set up by :mod:`.distributed`; by default the current device's.
+    """
+    t_start = time.perf_counter()
+    if not isinstance(k_pts, (int, np.integer)) or isinstance(k_pts, bool):
+        raise InvalidParameterError(f"k_pts must be an integer, got {k_pts!r}")
+    k_pts = int(k_pts)
+    if k_pts < 1:
+        raise InvalidParameterError(f"k_pts must be >= 1, got {k_pts}")
+    kind = _resolve_metric(metric)
+    if kind == "euclidean" and k_pts != 1:
+        raise InvalidParameterError("k_pts applies to the mrd metric only")
+    nthreads = _resolve_threads(threads)
+    if kind == "mrd":
+        raise InvalidParameterError("the mutual-reachability metric is not built for the B200 path yet "
+                                    "(SURVEY.md §8f row 1)")
+
+    p, n, d, flags, keep = _device_points(points)
+    flags |= (_lib.SUBTREE_SKIP if subtree_skip else 0) | (_lib.UPPER_BOUNDS if upper_bound_seeding else 0)
+    ne = n - 1
+    edges = np.empty((max(ne, 1), 2), np.int64)
+    weights = np.empty(max(ne, 1), np.float64)
+    st = _lib.Stats()
+    ctx = context if context is not None else _lib.default_context()
+    e = _lib.err_buf()
+    with ctx.lock:
+        rc = _lib.load().emst_boruvka(ctx.handle, p, n, d, flags, edges.ctypes.data, weights.ctypes.data,
+                                      ctypes.byref(st), e, len(e))
+    _lib.raise_for(rc, e)
+    edges = edges[:ne]
+    weights = weights[:ne]
+    total = time.perf_counter() - t_start
+    timings = {k: st.phase_ms[i] / 1e3 for i, k in enumerate(_lib.PHASES)}
+    timings["total"] = max(total, timings["tree"] + timings["core"] + timings["mst"])
+    return MstResult(
+        edges=edges,
+        weights=weights,
+        total_weight=float(np.sum(weights)),
+        iterations=int(st.iterations),
+        phase_timings=timings,
+        component_counts=[int(st.component_counts[i]) for i in range(st.num_counts)],
+        leaf_distance_evals=int(st.leaf_distance_evals),
+        threads=nthreads,
+        kernel_launches=int(st.kernel_launches),
+        gpus=int(st.world),
+    )
+
+
+# ----------------------------------------------------- per-round building blocks
+
+def reduce_labels(bvh: Bvh, state: ComponentState) -> np.ndarray:
+    """Internal-node labels, MIXED where children disagree (mst.py:436-448).
+
+    The GPU derives node labels from slot-range boundary counts over the tree it
+    builds from ``bvh.points`` (recorded by :func:`.bvh.build`).
+    """
+    if state.labels.shape[0] != bvh.num_points:
+        raise DimensionMismatchError("state does not match the hierarchy")
+    if bvh.points is None:
+        raise InvalidParameterError("reduce_labels needs a Bvh produced by build() (it carries its points)")
+    pts = as_point_array(bvh.points)
+    n = pts.shape[0]
+    if n > 1:
+        lab = np.ascontiguousarray(state.labels, np.int64)
+        out = np.empty(n - 1, np.int64)
+        ctx = _lib.default_context()
+        e = _lib.err_buf()
+        with ctx.lock:
+            rc = _lib.load().emst_reduce_labels(ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data,
+                                                out.ctypes.data, e, len(e))
+        _lib.raise_for(rc, e)
+        state.internal_labels[:] = out
+    return state.internal_labels
+
+
+def compute_upper_bounds(state: ComponentState, z_order, points, metric=None) -> np.ndarray:
+    """Seed radii from Z-adjacent cross-component pairs (mst.py:451-469)."""
+    pts = as_point_array(points)
+    n = pts.shape[0]
+    if state.labels.shape[0] != n or np.asarray(z_order).shape[0] != n:
+        raise DimensionMismatchError("state, order, and points disagree on size")
+    lab = np.ascontiguousarray(state.labels, np.int64)
+    ub = np.empty(n, np.float64)
+    ctx = _lib.default_context()
+    e = _lib.err_buf()
+    with ctx.lock:
+        rc = _lib.load().emst_compute_upper_bounds(ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data,
+                                                   ub.ctypes.data, e, len(e))
+    _lib.raise_for(rc, e)
+    state.upper_bounds[:] = ub
+    return state.upper_bounds
+
+
+def find_component_outgoing_edges(bvh: Bvh, points, state: ComponentState, metric=None, *,
+                                  subtree_skip: bool = True, use_upper_bounds: bool = True) -> OutgoingEdges:
+    """Cheapest edge leaving every live component (mst.py:472-514)."""
+    pts = as_point_array(points)
+    n = pts.shape[0]
+    if state.labels.shape[0] != n or pts.shape[1] != bvh.dim or bvh.num_points != n:
+        raise DimensionMismatchError("state does not match the hierarchy")
+    reps = np.unique(state.labels).astype(np.int64)
+    if reps.shape[0] < 2:
+        raise NothingToFindError("a single component has no outgoing edges")
+    lab = np.ascontiguousarray(state.labels, np.int64)
+    ub = np.ascontiguousarray(state.upper_bounds, np.float64)
+    bu = np.empty(n, np.int64)
+    bv = np.empty(n, np.int64)
+    bw = np.empty(n, np.float64)
+    evals = ctypes.c_int64(0)
+    flags = (_lib.SUBTREE_SKIP if subtree_skip else 0) | (_lib.UPPER_BOUNDS if use_upper_bounds else 0)
+    ctx = _lib.default_context()
+    e = _lib.err_buf()
+    with ctx.lock:
+        rc = _lib.load().emst_find_component_outgoing_edges(
+            ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data, ub.ctypes.data, flags, bu.ctypes.data,
+            bv.ctypes.data, bw.ctypes.data, ctypes.byref(evals), e, len(e))
+    _lib.raise_for(rc, e)
+    missing = reps[bv[reps] < 0]
+    if missing.shape[0] > 0:
+        raise NoOutgoingEdgeError(f"component {int(missing[0])} found no outgoing edge")
+    return OutgoingEdges(reps, bu, bv, bw, int(evals.value))
+
+
+def merge_components(state: ComponentState, outgoing: OutgoingEdges) -> MergeOutcome:
+    """Collapse the chosen-edge graph; relabel in place (mst.py:517-547)."""
+    reps = np.ascontiguousarray(outgoing.reps, np.int64)
+    n = state.labels.shape[0]
+    s = reps.shape[0]
+    lab = np.ascontiguousarray(state.labels, np.int64).copy()
+    ou = np.empty(max(s, 1), np.int64)
+    ov = np.empty(max(s, 1), np.int64)
+    ow = np.empty(max(s, 1), np.float64)
+    nr = np.empty(max(s, 1), np.int64)
+    ne = ctypes.c_int64(0)
+    nn = ctypes.c_int64(0)
+    bu = np.ascontiguousarray(outgoing.u, np.int64)
+    bv = np.ascontiguousarray(outgoing.v, np.int64)
+    bw = np.ascontiguousarray(outgoing.w, np.float64)
+    ctx = _lib.default_context()
+    e = _lib.err_buf()
+    with ctx.lock:
+        rc = _lib.load().emst_merge_components(ctx.handle, n, reps.ctypes.data, s, bu.ctypes.data, bv.ctypes.data,
+                                               bw.ctypes.data, lab.ctypes.data, ou.ctypes.data, ov.ctypes.data,
+                                               ow.ctypes.data, ctypes.byref(ne), nr.ctypes.data, ctypes.byref(nn),
+                                               e, len(e))
+    if rc == 5:
+        raise InternalInvariantViolation("a component's chosen edge is inconsistent")
+    _lib.raise_for(rc, e)
+    state.labels[:] = lab
+    k, m = ne.value, nn.value
+    return MergeOutcome(int(m), ou[:k].copy(), ov[:k].copy(), ow[:k].copy(), nr[:m].copy())
+
+
+def iteration_bound(n: int) -> int:
+    """ceil(log2 n) Boruvka rounds at most (mst.py:671)."""
+    return max(1, math.ceil(math.log2(n))) if n > 1 else 0
