@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""EMST throughput on B200: MFeatures/s = n*d / t / 1e6 (reference cli.py:100).
+
+One "step" is one full ``boruvka_emst`` of the synthetic cloud (build + all
+Boruvka rounds + final (w, u, v) edge sort), points resident in HBM before the
+timed region (``value``) or copied from pinned host memory with the edges read
+back inside it (``e2e``, through the public drop-in API).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config blobs3d_37m] [--impl ours|reference]
+
+N > 1 runs under torchrun, one process per GPU: every rank builds the same tree
+and takes a Morton slot range of each round's traversal; per-component minima
+meet in a two-phase NCCL min-allreduce (strong scaling: total work fixed).
+``--impl reference`` times the reference algorithm's CPU implementation (the C
+restatement in oracle/, all host threads) on a bounded sample of the same cloud.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+# BASELINE.json configs: name -> (kind, n, d, seed)
+CONFIGS = {
+    "blobs3d_37m": ("blobs", 37_000_000, 3, 0),     # configs[3], the headline (HACC-like)
+    "blobs2d_24m": ("blobs", 24_000_000, 2, 0),     # configs[4] (GeoLife-like)
+    "uniform2d_10m": ("uniform", 10_000_000, 2, 0), # configs[1]
+    "normal3d_10m": ("normal", 10_000_000, 3, 0),   # configs[2]
+    "uniform3d_100k": ("uniform", 100_000, 3, 0),   # configs[0]
+}
+METRIC = "MFeatures/s for EMST of 37M-pt 3D synthetic cloud, 1/2/4/8 B200; HBM GB/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0   # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+_THROTTLE = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+             0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(n: int, d: int, counts: list[int]) -> float:
+    """(24d+72)n + K(16d+84)n + 56*sum(c_k) + 48(n-1)."""
+    rounds = len(counts) - 1
+    return (24 * d + 72) * n + rounds * (16 * d + 84) * n + 56 * sum(counts[:-1]) + 48 * (n - 1)
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in _THROTTLE.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_points(cfg: str):
+    import paper_2207_00514_b200 as E
+    kind, n, d, seed = CONFIGS[cfg]
+    return E.generate(E.DatasetSpec(kind, n, d, seed))
+
+
+def cpu_sample(points, m: int):
+    import paper_2207_00514_b200 as E
+    return E.sample(points, min(m, points.shape[0]), 0)
+
+
+def time_oracle(points, m: int):
+    """Reference CPU algorithm (oracle/ C restatement, OpenMP on all host threads) on an m-point sample."""
+    from oracle import oracle as orc
+    sub = cpu_sample(points, m)
+    orc.set_threads(os.cpu_count() or 1)
+    t0 = time.perf_counter()
+    orc.boruvka_emst(sub)
+    dt = time.perf_counter() - t0
+    return sub.shape[0] * sub.shape[1] / dt / 1e6, dt, orc.num_threads(), sub.shape[0]
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    cfg = args.config
+    kind, n, d, seed = CONFIGS[cfg]
+    if rank != 0:
+        return
+    pts = make_points(cfg)
+    m = args.cpu_sample
+    rates = []
+    for i in range(args.warmup + args.steps):
+        rate, dt, threads, msz = time_oracle(pts, m)
+        if i >= args.warmup:
+            rates.append((rate, dt))
+    value = statistics.median(r for r, _ in rates)
+    ms = statistics.median(t for _, t in rates) * 1e3
+    sample = f"{m}-point uniform subsample (reference data.sample, seed 0) of the {cfg} cloud per step"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "MFeatures/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 coords / f64 weights", "data": "synthetic",
+        "config": {"workload": cfg, "kind": kind, "n": n, "d": d, "seed": seed, "sample_points": m},
+        "cpu_baseline": {"value": value, "unit": "MFeatures/s", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "MFeatures/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import paper_2207_00514_b200 as E
+
+    world, rank, local = dist_env()
+    cfg = args.config
+    kind, n, d, seed = CONFIGS[cfg]
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [E.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = E.Context(local, rank, world, obj[0])
+    else:
+        ctx = E.Context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream)
+
+    pts_host = make_points(cfg)
+    pts_dev = torch.from_numpy(pts_host).cuda()
+    edges = torch.empty((n - 1, 2), dtype=torch.int64, device="cuda")
+    weights = torch.empty((n - 1,), dtype=torch.float64, device="cuda")
+
+    def step():
+        return E.boruvka_emst_device(pts_dev, edges, weights, context=ctx)
+
+    for _ in range(args.warmup):
+        st = step()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    trav_ms = trav_launch = launches = 0
+    with ClockSampler(local) as clocks:
+        start.record(stream)
+        for _ in range(args.steps):
+            st = step()
+            trav_ms += st.traverse_ms
+            trav_launch += st.traverse_launches
+            launches += st.kernel_launches
+        end.record(stream)
+        torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = start.elapsed_time(end) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = n * d / (ms / 1e3) / 1e6
+    counts = [int(st.component_counts[i]) for i in range(st.num_counts)]
+
+    # end to end through the public drop-in: pinned host points in, host edges/weights out
+    pinned = torch.from_numpy(pts_host).pin_memory()
+    host_view = pinned.numpy()
+    e2e_ms = []
+    for i in range(max(2, min(args.steps, 3)) + 1):
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = E.boruvka_emst(host_view, context=ctx)
+        dt = (time.perf_counter() - t0) * 1e3
+        if i > 0:
+            e2e_ms.append(dt)
+    e2e = statistics.median(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([e2e], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+    assert res.component_counts == counts
+
+    peak, peak_src = hbm_peak()
+    # dominant kernel: the traversal; algorithmic bytes per query per round = 12d + 36
+    per_step_trav_ms = trav_ms / args.steps
+    trav_bytes = (12 * d + 36) * st.traverse_queries
+    trav_gbs = trav_bytes / (st.traverse_ms / 1e3) / 1e9 if st.traverse_ms > 0 else 0.0
+    whole_bytes = algorithmic_bytes(n, d, counts)
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "MFeatures/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 coords / f64 weights", "data": "synthetic (reference generator, seed 0)",
+        "config": {"workload": cfg, "kind": kind, "n": n, "d": d, "seed": seed,
+                   "parallelism": f"replicated tree, traversal sharded by Morton range x{world}",
+                   "l2": "inputs larger than L2 (points 444 MB + 2.4 GB tree at 37M), no flush"},
+        "e2e": {"value": n * d / (e2e / 1e3) / 1e6, "unit": "MFeatures/s", "ms_per_step": e2e,
+                "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": (n - 1) * 24},
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "kernel": "k_traverse", "achieved": trav_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": trav_gbs / peak, "traffic": None, "peak_source": peak_src,
+                     "bytes_model": f"(12d+36) B per query per round = {12 * d + 36} B",
+                     "launches_per_step": st.traverse_launches, "ms_per_step": per_step_trav_ms},
+        "whole_step_roofline": {"algorithmic_bytes": whole_bytes, "achieved_gbs": whole_bytes / (ms / 1e3) / 1e9,
+                                "frac": whole_bytes / (ms / 1e3) / 1e9 / (peak * world)},
+        "iterations": int(st.iterations), "component_counts": counts,
+        "phase_ms": {k: round(st.phase_ms[i], 3) for i, k in enumerate(E._lib.PHASES)},
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        rate, dt, threads, msz = time_oracle(pts_host, args.cpu_sample * 2)
+        line["cpu_baseline"] = {"value": rate, "unit": "MFeatures/s", "cores": threads, "kind": "port",
+                                "sample": f"{msz}-point subsample (data.sample seed 0) of {cfg}, {dt:.1f} s"}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="blobs3d_37m", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -73,6 +73,9 @@ typedef struct emst_stats {
   int64_t d2h_bytes;
   int32_t world;                /* GPUs that shared the traversal */
   int32_t rank;
+  double traverse_ms;           /* device time of the traversal kernel launches */
+  int64_t traverse_launches;
+  int64_t traverse_queries;     /* queries those launches processed (this rank) */
 } emst_stats;
 
 typedef struct emst_context emst_context;
@@ -87,6 +90,10 @@ int emst_nccl_unique_id(void* id_out_128, char* err, size_t errlen);
 int emst_context_create(int device, int rank, int world, const void* nccl_id, emst_context** out,
                         char* err, size_t errlen);
 int emst_context_destroy(emst_context* ctx);
+
+/* Run this context's work on an external CUDA stream (cudaStream_t; NULL restores
+ * the context's own stream) -- lets a caller time calls with its own events. */
+int emst_context_set_stream(emst_context* ctx, void* stream);
 
 /* Single-GPU shard emulation: split each round's traversal into `shards` Morton
  * ranges and combine them with the same two-phase min protocol the NCCL path

@@ -69,6 +69,9 @@ class Stats(ctypes.Structure):
         ("d2h_bytes", ctypes.c_int64),
         ("world", ctypes.c_int32),
         ("rank", ctypes.c_int32),
+        ("traverse_ms", ctypes.c_double),
+        ("traverse_launches", ctypes.c_int64),
+        ("traverse_queries", ctypes.c_int64),
     ]
 
 
@@ -76,6 +79,7 @@ EXPORTS = (
     "emst_nccl_unique_id",
     "emst_context_create",
     "emst_context_destroy",
+    "emst_context_set_stream",
     "emst_context_set_virtual_shards",
     "emst_boruvka",
     "emst_morton_codes",
@@ -118,6 +122,7 @@ def load():
         L.emst_context_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, ctypes.POINTER(vp), cp, sz]
         L.emst_context_destroy.argtypes = [vp]
         L.emst_context_set_virtual_shards.argtypes = [vp, ctypes.c_int]
+        L.emst_context_set_stream.argtypes = [vp, vp]
         L.emst_boruvka.argtypes = [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(Stats), cp, sz]
         L.emst_morton_codes.argtypes = [vp, vp, i64, i32, i32, vp, cp, sz]
         L.emst_build.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, cp, sz]
@@ -166,6 +171,11 @@ class Context:
         rc = load().emst_context_set_virtual_shards(self.handle, int(shards))
         if rc:
             raise InvalidParameterError(f"virtual shard count {shards} out of range [1, 64]")
+
+    def set_stream(self, stream) -> None:
+        """Run on an external CUDA stream (a torch.cuda.Stream or a raw cudaStream_t int; None = own)."""
+        handle = getattr(stream, "cuda_stream", stream)
+        load().emst_context_set_stream(self.handle, ctypes.c_void_p(handle) if handle else None)
 
     def close(self):
         if getattr(self, "handle", None) is not None and self.handle.value:

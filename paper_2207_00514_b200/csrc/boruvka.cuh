@@ -211,8 +211,10 @@ __global__ void k_merge_link(const int* __restrict__ succ, long long c, int* __r
 }
 
 // Find-with-path-halving to the root; concurrent halving only ever replaces a
-// pointer with one of its ancestors, so racing threads stay correct.
-__global__ void k_merge_jump(int* ptr, long long c, int* __restrict__ err) {
+// pointer with one of its ancestors, so racing threads stay correct.  The
+// result goes to root[k], which only thread k writes (ptr[k] itself may still
+// be overwritten by another thread's halving step).
+__global__ void k_merge_jump(int* ptr, long long c, int* __restrict__ root, int* __restrict__ err) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= c) return;
   volatile int* vp = ptr;
@@ -226,24 +228,24 @@ __global__ void k_merge_jump(int* ptr, long long c, int* __restrict__ err) {
     x = pp;
     if (++steps > c) { atomicOr(err, kErrChain); break; }
   }
-  vp[k] = x;
+  root[k] = x;
 }
 
 // flags packed for one scan: bit 0..30 "emits its edge", bit 31.. "is a root"
 struct MergeScanLoad {
   const int* succ;
-  const int* ptr;
+  const int* root;
   __device__ unsigned long long operator()(long long k) const {
     int y = succ[k];
     bool mutual = succ[y] == (int)k;
     unsigned long long edge = (mutual && y < (int)k) ? 0ull : 1ull;   // mst.py:416-423
-    unsigned long long root = ptr[k] == (int)k ? 1ull : 0ull;
-    return edge | (root << 31);
+    unsigned long long is_root = root[k] == (int)k ? 1ull : 0ull;
+    return edge | (is_root << 31);
   }
 };
 struct MergeScanStore {
   const int* succ;
-  const int* ptr;
+  const int* root;
   const EdgeKey* best;
   unsigned* eu;
   unsigned* ev;
@@ -260,14 +262,14 @@ struct MergeScanStore {
       ev[at] = (unsigned)(e.uv & 0xffffffffu);
       ew[at] = e.w;
     }
-    if (ptr[k] == (int)k) newid[k] = (int)(excl >> 31);
+    if (root[k] == (int)k) newid[k] = (int)(excl >> 31);
   }
 };
 
-__global__ void k_merge_final(const int* __restrict__ ptr, const int* __restrict__ newid, long long c, int* __restrict__ fin) {
+__global__ void k_merge_final(const int* __restrict__ root, const int* __restrict__ newid, long long c, int* __restrict__ fin) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= c) return;
-  fin[k] = newid[ptr[k]];
+  fin[k] = newid[root[k]];
 }
 
 __global__ void k_relabel(int* __restrict__ label, const int* __restrict__ fin, long long n) {

@@ -78,7 +78,11 @@ struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
   long long launches = 0;
+  double traverse_ms = 0.0;
+  long long traverse_launches = 0, traverse_queries = 0;
+  cudaEvent_t tv_a = nullptr, tv_b = nullptr;
   int num_sms = 148;
 
   // build
@@ -100,7 +104,7 @@ struct emst_context {
   DevBuf<int> label, bprefix;
   DevBuf<unsigned long long> ub;
   DevBuf<EdgeKey> best, shard_keys;
-  DevBuf<int> succ, ptr, newid, fin;
+  DevBuf<int> succ, ptr, root, newid, fin;
   DevBuf<unsigned> eu, ev;
   DevBuf<unsigned long long> ew;
   DevBuf<unsigned long long> xw, xuv;   // multi-GPU exchange
@@ -301,6 +305,7 @@ void ensure_rounds(emst_context* c, long long n) {
   c->best.ensure(n);
   c->succ.ensure(n);
   c->ptr.ensure(n);
+  c->root.ensure(n);
   c->newid.ensure(n);
   c->fin.ensure(n);
   c->eu.ensure(n);
@@ -348,10 +353,18 @@ template <int D, bool S, bool B>
 void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
   if (q1 <= q0) return;
   using Node = typename NodeOf<D>::type;
+  CK(cudaEventRecord(c->tv_a, c->stream));
   launch(c, k_traverse<D, S, B>, grid_for(q1 - q0, kTraverseThreads), kTraverseThreads, 0,
          (const Node*)reinterpret_cast<Node*>(c->nodes.p), (const float4*)c->spts.p, (const unsigned*)c->perm.p,
          (const int*)c->label.p, (const unsigned long long*)c->ub.p, out, q0, q1, (const Box3*)c->root_box.p,
          reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), reinterpret_cast<int*>(dev_counter(c, 3)));
+  CK(cudaEventRecord(c->tv_b, c->stream));
+  CK(cudaEventSynchronize(c->tv_b));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->tv_a, c->tv_b));
+  c->traverse_ms += ms;
+  c->traverse_launches++;
+  c->traverse_queries += q1 - q0;
 }
 
 void traverse_dispatch(emst_context* c, int flags, EdgeKey* out, long long q0, long long q1) {
@@ -399,11 +412,11 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
   launch(c, k_merge_succ, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, (const int*)c->label.p,
          (const unsigned*)c->iperm.p, c->succ.p, err);
   launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
-  launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, err);
-  MergeScanLoad load{c->succ.p, c->ptr.p};
-  MergeScanStore store{c->succ.p, c->ptr.p, c->best.p, c->eu.p, c->ev.p, c->ew.p, edge_base, c->newid.p};
+  launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, c->root.p, err);
+  MergeScanLoad load{c->succ.p, c->root.p};
+  MergeScanStore store{c->succ.p, c->root.p, c->best.p, c->eu.p, c->ev.p, c->ew.p, edge_base, c->newid.p};
   run_scan(c, comps, load, store, true);
-  launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->ptr.p, (const int*)c->newid.p, comps, c->fin.p);
+  launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->root.p, (const int*)c->newid.p, comps, c->fin.p);
   launch(c, k_relabel, grid_for(n, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
   read_counters(c);
   long long* h = c->host_counters;
@@ -549,7 +562,10 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     c->rank = rank;
     c->world = world;
     set_device(c);
-    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    CK(cudaEventCreate(&c->tv_a));
+    CK(cudaEventCreate(&c->tv_b));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaMallocHost(&c->host_counters, 8 * sizeof(long long)));
     CK(cudaEventCreate(&c->ev_a));
@@ -580,14 +596,22 @@ int emst_context_destroy(emst_context* c) {
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
   c->node_parent.release(); c->leaf_parent.release(); c->arrivals.release(); c->root_box.release();
   c->label.release(); c->bprefix.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
-  c->succ.release(); c->ptr.release(); c->newid.release(); c->fin.release();
+  c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->eu.release(); c->ev.release(); c->ew.release(); c->xw.release(); c->xuv.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
-  if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->tv_a) cudaEventDestroy(c->tv_a);
+  if (c->tv_b) cudaEventDestroy(c->tv_b);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
+  return EMST_OK;
+}
+
+int emst_context_set_stream(emst_context* c, void* stream) {
+  if (!c) return EMST_ERR_PARAM;
+  c->stream = stream ? reinterpret_cast<cudaStream_t>(stream) : c->own_stream;
   return EMST_OK;
 }
 
@@ -609,6 +633,9 @@ int emst_boruvka(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
     set_device(c);
     check_shape(n, d);
     const long long launches0 = c->launches;
+    c->traverse_ms = 0.0;
+    c->traverse_launches = 0;
+    c->traverse_queries = 0;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -654,6 +681,9 @@ int emst_boruvka(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     st->kernel_launches = c->launches - launches0;
+    st->traverse_ms = c->traverse_ms;
+    st->traverse_launches = c->traverse_launches;
+    st->traverse_queries = c->traverse_queries;
     return EMST_OK;
   } catch (const Failure& f) {
     if (f.code == EMST_ERR_NONFINITE) {
@@ -930,12 +960,12 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
     cmin.ensure(s);
     CK(cudaMemcpyAsync(dreps.p, reps, s * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(cmin.p, 0x7f, s * sizeof(long long), c->stream));
-    launch(c, k_cluster_min, grid_for(s, 256), 256, 0, (const int*)c->ptr.p, (const long long*)dreps.p, s, cmin.p);
+    launch(c, k_cluster_min, grid_for(s, 256), 256, 0, (const int*)c->root.p, (const long long*)dreps.p, s, cmin.p);
     std::vector<int> ptr(s), newlab(n);
     std::vector<long long> cm(s);
     std::vector<unsigned> eu(emitted), ev(emitted);
     std::vector<unsigned long long> ew(emitted);
-    CK(cudaMemcpyAsync(ptr.data(), c->ptr.p, s * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(ptr.data(), c->root.p, s * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(cm.data(), cmin.p, s * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     if (emitted) {
       CK(cudaMemcpyAsync(eu.data(), c->eu.p, emitted * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));

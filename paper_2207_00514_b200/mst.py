@@ -322,3 +322,31 @@ def merge_components(state: ComponentState, outgoing: OutgoingEdges) -> MergeOut
 def iteration_bound(n: int) -> int:
     """ceil(log2 n) Boruvka rounds at most (mst.py:671)."""
     return max(1, math.ceil(math.log2(n))) if n > 1 else 0
+
+
+def boruvka_emst_device(points, edges_out, weights_out, *, subtree_skip: bool = True,
+                        upper_bound_seeding: bool = True, context: _lib.Context | None = None) -> _lib.Stats:
+    """Device-resident variant: CUDA float32 points in, results written into CUDA tensors.
+
+    ``edges_out`` is an (n-1, 2) int64 CUDA tensor and ``weights_out`` an (n-1,)
+    float64 CUDA tensor; nothing crosses PCIe but the per-round control words.
+    Returns the raw run statistics.  Used by bench.py for the HBM-resident number.
+    """
+    import torch
+
+    if not (isinstance(points, torch.Tensor) and points.is_cuda and points.dtype == torch.float32):
+        raise InvalidParameterError("points must be a CUDA float32 tensor")
+    pts = points.contiguous()
+    n, d = int(pts.shape[0]), int(pts.shape[1])
+    if edges_out.shape != (max(n - 1, 0), 2) or weights_out.shape != (max(n - 1, 0),):
+        raise DimensionMismatchError("output tensors must be (n-1, 2) int64 and (n-1,) float64")
+    flags = _lib.POINTS_ON_DEVICE | _lib.OUTPUT_ON_DEVICE
+    flags |= (_lib.SUBTREE_SKIP if subtree_skip else 0) | (_lib.UPPER_BOUNDS if upper_bound_seeding else 0)
+    st = _lib.Stats()
+    ctx = context if context is not None else _lib.default_context()
+    e = _lib.err_buf()
+    with ctx.lock:
+        rc = _lib.load().emst_boruvka(ctx.handle, pts.data_ptr(), n, d, flags, edges_out.data_ptr(),
+                                      weights_out.data_ptr(), ctypes.byref(st), e, len(e))
+    _lib.raise_for(rc, e)
+    return st
