@@ -187,6 +187,11 @@ def run_ours(args):
     def step():
         return E.boruvka_emst_device(pts_dev, edges, weights, context=ctx)
 
+    if args.profile:
+        step()
+        torch.cuda.synchronize()
+        return
+
     for _ in range(args.warmup):
         st = step()
     if dist is not None:
@@ -281,6 +286,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="one untimed step only (for ncu); prints nothing")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
