@@ -19,6 +19,7 @@
 #pragma once
 #include "common.cuh"
 #include "scan.cuh"
+#include "traverse.cuh"
 
 namespace emst {
 
@@ -63,125 +64,6 @@ __global__ void k_node_labels(Node* __restrict__ nodes, const int2* __restrict__
   int ll = bg == bl ? label[r.x] : kMixed;
   int rl = bh == bg1 ? label[r.y] : kMixed;
   *reinterpret_cast<int2*>(&nodes[i].ref.z) = make_int2(ll, rl);
-}
-
-// ---------------------------------------------------------------- traversal
-template <int D>
-__device__ __forceinline__ void child_box(const Node3& rec, int side, float* lo, float* hi) {
-  if (side == 0) {
-    lo[0] = rec.a.x; lo[1] = rec.a.y; lo[2] = rec.a.z; hi[0] = rec.a.w; hi[1] = rec.b.x; hi[2] = rec.b.y;
-  } else {
-    lo[0] = rec.b.z; lo[1] = rec.b.w; lo[2] = rec.c.x; hi[0] = rec.c.y; hi[1] = rec.c.z; hi[2] = rec.c.w;
-  }
-}
-template <int D>
-__device__ __forceinline__ void child_box(const Node2& rec, int side, float* lo, float* hi) {
-  const float4& v = side == 0 ? rec.a : rec.b;
-  lo[0] = v.x; lo[1] = v.y; hi[0] = v.z; hi[1] = v.w; lo[2] = hi[2] = 0.f;
-}
-
-__device__ __forceinline__ Node3 load_node(const Node3* p) {
-  const float4* f = reinterpret_cast<const float4*>(p);
-  Node3 r;
-  r.a = __ldg(f);
-  r.b = __ldg(f + 1);
-  r.c = __ldg(f + 2);
-  r.ref = __ldg(reinterpret_cast<const int4*>(f + 3));
-  return r;
-}
-__device__ __forceinline__ Node2 load_node(const Node2* p) {
-  const float4* f = reinterpret_cast<const float4*>(p);
-  Node2 r;
-  r.a = __ldg(f);
-  r.b = __ldg(f + 1);
-  r.ref = __ldg(reinterpret_cast<const int4*>(f + 2));
-  return r;
-}
-
-constexpr int kTraverseThreads = 256;
-
-template <int D, bool kSkip, bool kBounds>
-__global__ void __launch_bounds__(kTraverseThreads)
-k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
-           const unsigned* __restrict__ perm, const int* __restrict__ label,
-           const unsigned long long* __restrict__ ub, EdgeKey* __restrict__ best, long long q0, long long q1,
-           const Box3* __restrict__ root_box, unsigned long long* __restrict__ evals_out, int* __restrict__ overflow) {
-  const long long s = q0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  unsigned long long evals = 0;
-  if (s < q1) {
-    const float4 qv = spts[s];
-    const float q[3] = {qv.x, qv.y, qv.z};
-    const unsigned qp = __float_as_uint(qv.w);
-    const int comp = label[s];
-    double radius = kBounds ? bits_to_radius(ub[comp]) : __longlong_as_double(0x7ff0000000000000ll);
-    float r2 = prune_r2(radius);
-    unsigned long long best_w = ~0ull, best_uv = ~0ull;
-
-    int stack_node[kStackCapacity];
-    float stack_lb[kStackCapacity];
-    stack_node[0] = 0;
-    stack_lb[0] = box_lb2<D>(q, root_box->lo, root_box->hi);
-    int top = 1;
-    while (top > 0) {
-      --top;
-      if (stack_lb[top] > r2) continue;
-      const auto rec = load_node(nodes + stack_node[top]);
-      int push_node[2];
-      float push_lb[2];
-      int np = 0;
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int c = side ? rec.ref.y : rec.ref.x;
-        const int cl = side ? rec.ref.w : rec.ref.z;
-        float lo[3], hi[3];
-        child_box<D>(rec, side, lo, hi);
-        if (c < 0) {
-          if (cl == comp) continue;
-          ++evals;
-          const double w = exact_dist<D>(q, lo);
-          if (w <= radius) {
-            const unsigned p = __ldg(perm + (~c));
-            const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
-            const unsigned long long uv = (u << 32) | v;
-            const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
-            if (key_less(wb, uv, best_w, best_uv)) {
-              best_w = wb;
-              best_uv = uv;
-              radius = w;
-              r2 = prune_r2(w);
-            }
-          }
-        } else {
-          if (kSkip && cl == comp) continue;
-          const float lb = box_lb2<D>(q, lo, hi);
-          if (lb <= r2) {
-            push_node[np] = c;
-            push_lb[np] = lb;
-            ++np;
-          }
-        }
-      }
-      if (np == 2) {
-        if (top + 2 > kStackCapacity) { atomicOr(overflow, 1); break; }
-        // nearer child on top (popped first); ties keep the left child there
-        const int near = push_lb[1] < push_lb[0] ? 1 : 0;
-        stack_node[top] = push_node[1 - near];
-        stack_lb[top] = push_lb[1 - near];
-        stack_node[top + 1] = push_node[near];
-        stack_lb[top + 1] = push_lb[near];
-        top += 2;
-      } else if (np == 1) {
-        if (top + 1 > kStackCapacity) { atomicOr(overflow, 1); break; }
-        stack_node[top] = push_node[0];
-        stack_lb[top] = push_lb[0];
-        ++top;
-      }
-    }
-    if (best_uv != ~0ull) atomic_min_key(&best[comp], best_w, best_uv);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
-  if (lane_id() == 0 && evals) atomicAdd(evals_out, evals);
 }
 
 // ------------------------------------------------------------------- merge

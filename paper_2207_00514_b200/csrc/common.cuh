@@ -78,17 +78,18 @@ __device__ __forceinline__ double exact_dist(const float* q, const float* p) {
   return __dsqrt_rn(s);
 }
 
-// Conservative squared lower bound from q to a box in f32, every operation
-// rounded toward -inf so it never exceeds the exact squared distance.
+// Conservative squared lower bound from q to a box in f32: the per-axis gap
+// max(0, lo - q, q - hi) and the sum of squares are all rounded toward -inf,
+// so the result never exceeds the exact squared distance (overflow saturates
+// at FLT_MAX, still a lower bound).  A leaf is a degenerate box (lo == hi == p),
+// for which this is a lower bound on |q - p|^2.
 template <int D>
 __device__ __forceinline__ float box_lb2(const float* q, const float* lo, const float* hi) {
   float s = 0.f;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    float g = 0.f;
-    if (q[k] < lo[k]) g = __fsub_rd(lo[k], q[k]);
-    else if (q[k] > hi[k]) g = __fsub_rd(q[k], hi[k]);
-    s = __fadd_rd(s, __fmul_rd(g, g));
+    float g = fmaxf(0.f, fmaxf(__fsub_rd(lo[k], q[k]), __fsub_rd(q[k], hi[k])));
+    s = __fmaf_rd(g, g, s);
   }
   return s;
 }

@@ -353,11 +353,19 @@ template <int D, bool S, bool B>
 void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
   if (q1 <= q0) return;
   using Node = typename NodeOf<D>::type;
+  auto kernel = k_traverse<D, S, B>;
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTraverseThreads, 0));
+  const long long warps_needed = (q1 - q0 + kTraverseChunk - 1) / kTraverseChunk;
+  const long long blocks_needed = (warps_needed + kTraverseThreads / 32 - 1) / (kTraverseThreads / 32);
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((long long)c->num_sms * std::max(per_sm, 1),
+                                                                             blocks_needed));
+  unsigned long long* work = reinterpret_cast<unsigned long long*>(dev_counter(c, 4));
+  CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
   CK(cudaEventRecord(c->tv_a, c->stream));
-  launch(c, k_traverse<D, S, B>, grid_for(q1 - q0, kTraverseThreads), kTraverseThreads, 0,
-         (const Node*)reinterpret_cast<Node*>(c->nodes.p), (const float4*)c->spts.p, (const unsigned*)c->perm.p,
-         (const int*)c->label.p, (const unsigned long long*)c->ub.p, out, q0, q1, (const Box3*)c->root_box.p,
-         reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), reinterpret_cast<int*>(dev_counter(c, 3)));
+  launch(c, kernel, grid, kTraverseThreads, 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p), (const float4*)c->spts.p,
+         (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1, (const Box3*)c->root_box.p,
+         reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), reinterpret_cast<int*>(dev_counter(c, 3)), work);
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
   float ms = 0.f;

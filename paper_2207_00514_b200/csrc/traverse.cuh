@@ -1,0 +1,212 @@
+// traverse.cuh -- the hot kernel: per-query constrained nearest-foreign-neighbour
+// search, Algorithm 2 of the paper (reference mst.py:227-328).
+//
+// B200 design:
+//   * persistent warps with lane refill: a lane that finishes its query takes
+//     the next one from its warp's chunk of consecutive Morton slots, so warps
+//     no longer idle behind their longest query (warp max/mean pops is 1.7-1.9);
+//   * one 64-byte node record per pop carries both child boxes, child refs and
+//     child component labels (leaf children as degenerate boxes), fetched with
+//     four 16-byte loads through the read-only path;
+//   * both children get the same branch-free conservative f32 lower bound
+//     (rounded toward -inf); only leaves that survive it pay for the exact f64
+//     reference distance (bvh.py:284-290) that decides acceptance;
+//   * the per-component radius is shared: an accepted leaf lowers ub[comp] with
+//     a u64 atomicMin on the f64 bit pattern and every lane re-reads it every
+//     16 pops.  Any value written is a real outgoing edge of the component, so
+//     the radius never drops below the component's minimum -- the result is
+//     unchanged ("in the extreme case ...").
+//   * per-component result: 128-bit atomic min of (w bits, u << 32 | v).
+#pragma once
+#include "common.cuh"
+
+namespace emst {
+
+template <int D>
+__device__ __forceinline__ void child_box(const Node3& rec, int side, float* lo, float* hi) {
+  if (side == 0) {
+    lo[0] = rec.a.x; lo[1] = rec.a.y; lo[2] = rec.a.z; hi[0] = rec.a.w; hi[1] = rec.b.x; hi[2] = rec.b.y;
+  } else {
+    lo[0] = rec.b.z; lo[1] = rec.b.w; lo[2] = rec.c.x; hi[0] = rec.c.y; hi[1] = rec.c.z; hi[2] = rec.c.w;
+  }
+}
+template <int D>
+__device__ __forceinline__ void child_box(const Node2& rec, int side, float* lo, float* hi) {
+  const float4& v = side == 0 ? rec.a : rec.b;
+  lo[0] = v.x; lo[1] = v.y; hi[0] = v.z; hi[1] = v.w; lo[2] = hi[2] = 0.f;
+}
+
+__device__ __forceinline__ Node3 load_node(const Node3* p) {
+  const float4* f = reinterpret_cast<const float4*>(p);
+  Node3 r;
+  r.a = __ldg(f);
+  r.b = __ldg(f + 1);
+  r.c = __ldg(f + 2);
+  r.ref = __ldg(reinterpret_cast<const int4*>(f + 3));
+  return r;
+}
+__device__ __forceinline__ Node2 load_node(const Node2* p) {
+  const float4* f = reinterpret_cast<const float4*>(p);
+  Node2 r;
+  r.a = __ldg(f);
+  r.b = __ldg(f + 1);
+  r.ref = __ldg(reinterpret_cast<const int4*>(f + 2));
+  return r;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt_u32() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+constexpr int kTraverseThreads = 256;
+constexpr int kTraverseChunk = 128;     // consecutive Morton queries a warp claims at once
+constexpr int kRefillIdle = 8;          // refill when this many lanes are idle (or all are)
+constexpr int kRadiusRefresh = 16;      // pops between re-reads of the shared radius
+
+template <int D, bool kSkip, bool kBounds>
+__global__ void __launch_bounds__(kTraverseThreads, 4)
+k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
+           const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
+           EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
+           unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
+           unsigned long long* __restrict__ work_counter) {
+  const unsigned lane = lane_id();
+  const unsigned lt = lanemask_lt_u32();
+  const long long total = q1 - q0;
+  float rlo[3], rhi[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) { rlo[k] = root_box->lo[k]; rhi[k] = root_box->hi[k]; }
+
+  long long pool_next = 0, pool_end = 0;   // warp-uniform chunk of claimed queries
+  bool exhausted = false;                  // warp-uniform: global work is gone
+
+  long long s = -1;
+  float q[3] = {0.f, 0.f, 0.f};
+  unsigned qp = 0;
+  int comp = 0;
+  double radius = 0.0;
+  float r2 = 0.f;
+  unsigned long long best_w = ~0ull, best_uv = ~0ull;
+  int stack_node[kStackCapacity];
+  float stack_lb[kStackCapacity];
+  int top = 0;
+  int since_refresh = 0;
+  unsigned long long evals = 0;
+
+  for (;;) {
+    // ---- refill idle lanes from the warp's chunk of consecutive Morton slots
+    const unsigned idle = __ballot_sync(0xffffffffu, s < 0);
+    const int n_idle = __popc(idle);
+    if (n_idle == 32 && exhausted) break;
+    if (n_idle >= kRefillIdle || n_idle == 32) {           // warp-uniform
+      if (pool_next >= pool_end && !exhausted) {
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(work_counter, (unsigned long long)kTraverseChunk);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if ((long long)base >= total) {
+          exhausted = true;
+        } else {
+          pool_next = (long long)base;
+          pool_end = min((long long)base + kTraverseChunk, total);
+        }
+      }
+      if (pool_next < pool_end) {
+        const unsigned rank = __popc(idle & lt);
+        const long long mine = pool_next + (long long)rank;
+        const bool take = s < 0 && mine < pool_end;
+        pool_next = min(pool_end, pool_next + (long long)n_idle);
+        if (take) {
+          s = mine;
+          const long long slot = q0 + s;
+          const float4 qv = spts[slot];
+          q[0] = qv.x; q[1] = qv.y; q[2] = qv.z;
+          qp = __float_as_uint(qv.w);
+          comp = label[slot];
+          radius = kBounds ? bits_to_radius(__ldcg(&ub[comp])) : __longlong_as_double(0x7ff0000000000000ll);
+          r2 = prune_r2(radius);
+          best_w = ~0ull;
+          best_uv = ~0ull;
+          stack_node[0] = 0;
+          stack_lb[0] = box_lb2<D>(q, rlo, rhi);
+          top = 1;
+          since_refresh = 0;
+        }
+      }
+    }
+    if (s < 0) continue;
+
+    // ---- one pop
+    --top;
+    const float plb = stack_lb[top];
+    if (kBounds && ++since_refresh >= kRadiusRefresh) {
+      since_refresh = 0;
+      const double shared = bits_to_radius(__ldcg(&ub[comp]));
+      if (shared < radius) { radius = shared; r2 = prune_r2(shared); }
+    }
+    if (plb <= r2) {
+      const auto rec = load_node(nodes + stack_node[top]);
+      float lbs[2];
+      bool want[2];
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int c = side ? rec.ref.y : rec.ref.x;
+        const int cl = side ? rec.ref.w : rec.ref.z;
+        float lo[3], hi[3];
+        child_box<D>(rec, side, lo, hi);
+        lbs[side] = box_lb2<D>(q, lo, hi);
+        // leaves are always skipped when they are in the query's component (mst.py:276);
+        // internal subtrees only under subtree skipping (mst.py:291)
+        const bool same = cl == comp && (c < 0 || kSkip);
+        want[side] = !same && lbs[side] <= r2;
+        if (want[side] && c < 0) {
+          want[side] = false;
+          ++evals;
+          const double w = exact_dist<D>(q, lo);
+          if (w <= radius) {
+            const unsigned p = __ldg(perm + (~c));
+            const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
+            const unsigned long long uv = (u << 32) | v;
+            const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
+            if (key_less(wb, uv, best_w, best_uv)) {
+              best_w = wb;
+              best_uv = uv;
+              if (w < radius) {
+                radius = w;
+                r2 = prune_r2(w);
+                if (kBounds) atomicMin(&ub[comp], wb);
+              }
+            }
+          }
+        }
+      }
+      const int np = (int)want[0] + (int)want[1];
+      if (top + np > kStackCapacity) {
+        atomicOr(overflow, 1);
+        top = 0;
+      } else if (np == 2) {
+        // nearer child on top (popped first); ties keep the left child there
+        const int near = lbs[1] < lbs[0] ? 1 : 0;
+        stack_node[top] = near ? rec.ref.x : rec.ref.y;
+        stack_lb[top] = lbs[1 - near];
+        stack_node[top + 1] = near ? rec.ref.y : rec.ref.x;
+        stack_lb[top + 1] = lbs[near];
+        top += 2;
+      } else if (np == 1) {
+        stack_node[top] = want[0] ? rec.ref.x : rec.ref.y;
+        stack_lb[top] = want[0] ? lbs[0] : lbs[1];
+        ++top;
+      }
+    }
+    if (top == 0) {
+      if (best_uv != ~0ull) atomic_min_key(&best[comp], best_w, best_uv);
+      s = -1;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+  if (lane == 0 && evals) atomicAdd(evals_out, evals);
+}
+
+}  // namespace emst
