@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -76,6 +77,7 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
+  int traversal = 1;   // 0 = per-lane persistent, 1 = warp packet (EMST_TRAVERSAL=lane|packet)
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
@@ -363,9 +365,17 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
   unsigned long long* work = reinterpret_cast<unsigned long long*>(dev_counter(c, 4));
   CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
   CK(cudaEventRecord(c->tv_a, c->stream));
-  launch(c, kernel, grid, kTraverseThreads, 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p), (const float4*)c->spts.p,
-         (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1, (const Box3*)c->root_box.p,
-         reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), reinterpret_cast<int*>(dev_counter(c, 3)), work);
+  if (c->traversal == 1) {
+    launch(c, k_traverse_packet<D, S, B>, grid_for(q1 - q0, kTraverseThreads), kTraverseThreads, 0,
+           (const Node*)reinterpret_cast<Node*>(c->nodes.p), (const float4*)c->spts.p, (const unsigned*)c->perm.p,
+           (const int*)c->label.p, c->ub.p, out, q0, q1, (const Box3*)c->root_box.p,
+           reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), reinterpret_cast<int*>(dev_counter(c, 3)));
+  } else {
+    launch(c, kernel, grid, kTraverseThreads, 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p),
+           (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
+           (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
+           reinterpret_cast<int*>(dev_counter(c, 3)), work);
+  }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
   float ms = 0.f;
@@ -567,6 +577,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (world < 1 || rank < 0 || rank >= world) fail(EMST_ERR_PARAM, "bad rank %d / world %d", rank, world);
     c = new emst_context();
     c->device = device;
+    if (const char* t = getenv("EMST_TRAVERSAL")) c->traversal = strcmp(t, "lane") == 0 ? 0 : 1;
     c->rank = rank;
     c->world = world;
     set_device(c);

@@ -209,4 +209,136 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   if (lane == 0 && evals) atomicAdd(evals_out, evals);
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-packet variant: the 32 lanes of a warp hold 32 consecutive Morton
+// queries and walk ONE shared stack.  A node is visited once per warp (one
+// broadcast 64-byte fetch) and tested by every lane against its own query,
+// radius and component; a child is pushed when any lane still needs it, and
+// each lane keeps its own lower bound per stack entry (NaN = "not for me").
+// Control flow is warp-uniform except the exact f64 leaf test, so SIMT
+// efficiency no longer depends on how different the lanes' path lengths are.
+constexpr int kPacketWarps = kTraverseThreads / 32;
+
+template <int D, bool kSkip, bool kBounds>
+__global__ void __launch_bounds__(kTraverseThreads, 4)
+k_traverse_packet(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
+                  const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
+                  EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
+                  unsigned long long* __restrict__ evals_out, int* __restrict__ overflow) {
+  __shared__ int s_stack[kPacketWarps][kStackCapacity];
+  const unsigned lane = lane_id();
+  const int wib = threadIdx.x >> 5;
+  int* stack_node = s_stack[wib];
+  const long long s = q0 + (blockIdx.x * (long long)kPacketWarps + wib) * 32 + lane;
+  const bool valid = s < q1;
+  if (__ballot_sync(0xffffffffu, valid) == 0) return;
+
+  float q[3] = {0.f, 0.f, 0.f};
+  unsigned qp = 0;
+  int comp = kMixed - 1;   // matches no label
+  double radius = -1.0;
+  float r2 = -1.f;
+  if (valid) {
+    const float4 qv = spts[s];
+    q[0] = qv.x; q[1] = qv.y; q[2] = qv.z;
+    qp = __float_as_uint(qv.w);
+    comp = label[s];
+    radius = kBounds ? bits_to_radius(__ldcg(&ub[comp])) : __longlong_as_double(0x7ff0000000000000ll);
+    r2 = prune_r2(radius);
+  }
+  unsigned long long best_w = ~0ull, best_uv = ~0ull;
+  float stack_lb[kStackCapacity];
+  const float kNone = __int_as_float(0x7fc00000);   // NaN: never <= r2
+  {
+    float rlo[3], rhi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { rlo[k] = root_box->lo[k]; rhi[k] = root_box->hi[k]; }
+    stack_lb[0] = valid ? box_lb2<D>(q, rlo, rhi) : kNone;
+  }
+  if (lane == 0) stack_node[0] = 0;
+  __syncwarp();
+  int top = 1;
+  int since_refresh = 0;
+  unsigned long long evals = 0;
+
+  while (top > 0) {
+    --top;
+    const int node = stack_node[top];
+    if (kBounds && valid && ++since_refresh >= kRadiusRefresh) {
+      since_refresh = 0;
+      const double shared = bits_to_radius(__ldcg(&ub[comp]));
+      if (shared < radius) { radius = shared; r2 = prune_r2(shared); }
+    }
+    const bool active = stack_lb[top] <= r2;
+    if (!__any_sync(0xffffffffu, active)) continue;
+    const auto rec = load_node(nodes + node);
+    float lbs[2];
+    bool want[2];
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int c = side ? rec.ref.y : rec.ref.x;
+      const int cl = side ? rec.ref.w : rec.ref.z;
+      float lo[3], hi[3];
+      child_box<D>(rec, side, lo, hi);
+      lbs[side] = box_lb2<D>(q, lo, hi);
+      const bool same = cl == comp && (c < 0 || kSkip);
+      want[side] = active && !same && lbs[side] <= r2;
+      if (c < 0) {   // warp-uniform: leaf child
+        if (want[side]) {
+          ++evals;
+          const double w = exact_dist<D>(q, lo);
+          if (w <= radius) {
+            const unsigned p = __ldg(perm + (~c));
+            const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
+            const unsigned long long uv = (u << 32) | v;
+            const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
+            if (key_less(wb, uv, best_w, best_uv)) {
+              best_w = wb;
+              best_uv = uv;
+              if (w < radius) {
+                radius = w;
+                r2 = prune_r2(w);
+                if (kBounds) atomicMin(&ub[comp], wb);
+              }
+            }
+          }
+        }
+        want[side] = false;
+      }
+    }
+    const unsigned m0 = __ballot_sync(0xffffffffu, want[0]);
+    const unsigned m1 = __ballot_sync(0xffffffffu, want[1]);
+    const int np = (m0 != 0) + (m1 != 0);
+    if (np == 0) continue;
+    if (top + np > kStackCapacity) {
+      if (lane == 0) atomicOr(overflow, 1);
+      break;
+    }
+    __syncwarp();
+    if (np == 2) {
+      // nearer child on top for the majority of the lanes that need either
+      const unsigned vote = __ballot_sync(0xffffffffu, (want[0] || want[1]) && lbs[1] < lbs[0]);
+      const int near = 2 * __popc(vote) > __popc(m0 | m1) ? 1 : 0;
+      if (lane == 0) {
+        stack_node[top] = near ? rec.ref.x : rec.ref.y;
+        stack_node[top + 1] = near ? rec.ref.y : rec.ref.x;
+      }
+      stack_lb[top] = want[1 - near] ? lbs[1 - near] : kNone;
+      stack_lb[top + 1] = want[near] ? lbs[near] : kNone;
+      top += 2;
+    } else {
+      const int side = m0 ? 0 : 1;
+      if (lane == 0) stack_node[top] = side ? rec.ref.y : rec.ref.x;
+      stack_lb[top] = want[side] ? lbs[side] : kNone;
+      ++top;
+    }
+    __syncwarp();
+  }
+  if (valid && best_uv != ~0ull) atomic_min_key(&best[comp], best_w, best_uv);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+  if (lane == 0 && evals) atomicAdd(evals_out, evals);
+}
+
 }  // namespace emst
