@@ -26,7 +26,7 @@ from .errors import (
 )
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libemst_b200.so")
+LIB_PATH = os.environ.get("EMST_LIB_PATH") or os.path.join(PKG_DIR, "libemst_b200.so")
 CSRC = os.path.join(PKG_DIR, "csrc")
 
 SUBTREE_SKIP = 1

@@ -40,8 +40,10 @@ struct RoundScanLoad {
       float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
       double w = dim == 3 ? exact_dist<3>(pa, pb) : exact_dist<2>(pa, pb);
       unsigned long long bits = (unsigned long long)__double_as_longlong(w);
-      atomicMin(&ub[la], bits);
-      atomicMin(&ub[lb], bits);
+      // late rounds funnel many boundary pairs into few components: read first,
+      // and only issue the atomic when it can still lower the bound
+      if (bits < __ldcg(&ub[la])) atomicMin(&ub[la], bits);
+      if (bits < __ldcg(&ub[lb])) atomicMin(&ub[lb], bits);
     }
     return 1ull;
   }

@@ -77,7 +77,7 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
-  int traversal = 1;   // 0 = per-lane persistent, 1 = warp packet (EMST_TRAVERSAL=lane|packet)
+  int traversal = 0;   // 0 = per-lane persistent, 1 = warp packet (EMST_TRAVERSAL=lane|packet)
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
@@ -577,7 +577,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (world < 1 || rank < 0 || rank >= world) fail(EMST_ERR_PARAM, "bad rank %d / world %d", rank, world);
     c = new emst_context();
     c->device = device;
-    if (const char* t = getenv("EMST_TRAVERSAL")) c->traversal = strcmp(t, "lane") == 0 ? 0 : 1;
+    if (const char* t = getenv("EMST_TRAVERSAL")) c->traversal = strcmp(t, "packet") == 0 ? 1 : 0;
     c->rank = rank;
     c->world = world;
     set_device(c);

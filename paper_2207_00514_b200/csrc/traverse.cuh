@@ -36,13 +36,20 @@ __device__ __forceinline__ void child_box(const Node2& rec, int side, float* lo,
   lo[0] = v.x; lo[1] = v.y; hi[0] = v.z; hi[1] = v.w; lo[2] = hi[2] = 0.f;
 }
 
+// 256-bit read-only loads (LDG.E.ENL2.256 on sm_100a): a 64-byte Node3 is two
+// load instructions instead of four.  Node records are immutable during a launch.
+__device__ __forceinline__ void ldg256(const void* p, float4& lo, float4& hi) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(lo.x), "=f"(lo.y), "=f"(lo.z), "=f"(lo.w), "=f"(hi.x), "=f"(hi.y), "=f"(hi.z), "=f"(hi.w)
+               : "l"(p));
+}
 __device__ __forceinline__ Node3 load_node(const Node3* p) {
   const float4* f = reinterpret_cast<const float4*>(p);
   Node3 r;
-  r.a = __ldg(f);
-  r.b = __ldg(f + 1);
-  r.c = __ldg(f + 2);
-  r.ref = __ldg(reinterpret_cast<const int4*>(f + 3));
+  float4 refs;
+  ldg256(f, r.a, r.b);
+  ldg256(f + 2, r.c, refs);
+  r.ref = make_int4(__float_as_int(refs.x), __float_as_int(refs.y), __float_as_int(refs.z), __float_as_int(refs.w));
   return r;
 }
 __device__ __forceinline__ Node2 load_node(const Node2* p) {
@@ -61,12 +68,18 @@ __device__ __forceinline__ unsigned lanemask_lt_u32() {
 }
 
 constexpr int kTraverseThreads = 256;
+#ifndef EMST_TRAV_MINB
+#define EMST_TRAV_MINB 4
+#endif
+#ifndef EMST_REFILL_IDLE
+#define EMST_REFILL_IDLE 8
+#endif
 constexpr int kTraverseChunk = 128;     // consecutive Morton queries a warp claims at once
-constexpr int kRefillIdle = 8;          // refill when this many lanes are idle (or all are)
+constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
 constexpr int kRadiusRefresh = 16;      // pops between re-reads of the shared radius
 
 template <int D, bool kSkip, bool kBounds>
-__global__ void __launch_bounds__(kTraverseThreads, 4)
+__global__ void __launch_bounds__(kTraverseThreads, EMST_TRAV_MINB)
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
