@@ -78,7 +78,7 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
-  int traversal = 0;   // EMST_TRAVERSAL: 0 lane (binary), 1 packet (binary), 2 wide4, 3 wide8
+  int traversal = 2;   // EMST_TRAVERSAL: 0 lane (binary), 1 packet (binary), 2 wide4, 3 wide8
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
@@ -651,7 +651,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     c = new emst_context();
     c->device = device;
     if (const char* t = getenv("EMST_TRAVERSAL"))
-      c->traversal = !strcmp(t, "wide4") ? 2 : !strcmp(t, "packet") ? 1 : !strcmp(t, "wide8") ? 3 : 0;
+      c->traversal = !strcmp(t, "lane") ? 0 : !strcmp(t, "packet") ? 1 : !strcmp(t, "wide8") ? 3 : 2;
     c->rank = rank;
     c->world = world;
     set_device(c);

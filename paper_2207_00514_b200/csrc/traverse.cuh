@@ -105,7 +105,6 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   int stack_node[kStackCapacity];
   float stack_lb[kStackCapacity];
   int top = 0;
-  int cur = -1;   // node being visited (kept out of the stack)
   int since_refresh = 0;
   unsigned long long evals = 0;
 
@@ -142,86 +141,80 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           r2 = prune_r2(radius);
           best_w = ~0ull;
           best_uv = ~0ull;
-          top = 0;
-          cur = box_lb2<D>(q, rlo, rhi) <= r2 ? 0 : -1;
+          stack_node[0] = 0;
+          stack_lb[0] = box_lb2<D>(q, rlo, rhi);
+          top = 1;
           since_refresh = 0;
         }
       }
     }
     if (s < 0) continue;
 
-    // ---- next node: the near child kept in a register, else pop (skipping entries
-    //      the radius has since pruned); an empty stack finishes the query
-    if (cur < 0) {
-      while (top > 0) {
-        --top;
-        if (stack_lb[top] <= r2) { cur = stack_node[top]; break; }
-      }
-      if (cur < 0) {
-        if (best_uv != ~0ull) atomic_min_key(&best[comp], best_w, best_uv);
-        s = -1;
-        continue;
-      }
-    }
+    // ---- one pop
+    --top;
+    const float plb = stack_lb[top];
     if (kBounds && ++since_refresh >= kRadiusRefresh) {
       since_refresh = 0;
       const double shared = bits_to_radius(__ldcg(&ub[comp]));
       if (shared < radius) { radius = shared; r2 = prune_r2(shared); }
     }
-    const auto rec = load_node(nodes + cur);
-    float lbs[2];
-    bool want[2];
+    if (plb <= r2) {
+      const auto rec = load_node(nodes + stack_node[top]);
+      float lbs[2];
+      bool want[2];
 #pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const int c = side ? rec.ref.y : rec.ref.x;
-      const int cl = side ? rec.ref.w : rec.ref.z;
-      float lo[3], hi[3];
-      child_box<D>(rec, side, lo, hi);
-      lbs[side] = box_lb2<D>(q, lo, hi);
-      // leaves are always skipped when they are in the query's component (mst.py:276);
-      // internal subtrees only under subtree skipping (mst.py:291)
-      const bool same = cl == comp && (c < 0 || kSkip);
-      want[side] = !same && lbs[side] <= r2;
-      if (want[side] && c < 0) {
-        want[side] = false;
-        ++evals;
-        const double w = exact_dist<D>(q, lo);
-        if (w <= radius) {
-          const unsigned p = __ldg(perm + (~c));
-          const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
-          const unsigned long long uv = (u << 32) | v;
-          const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
-          if (key_less(wb, uv, best_w, best_uv)) {
-            best_w = wb;
-            best_uv = uv;
-            if (w < radius) {
-              radius = w;
-              r2 = prune_r2(w);
-              if (kBounds) atomicMin(&ub[comp], wb);
+      for (int side = 0; side < 2; ++side) {
+        const int c = side ? rec.ref.y : rec.ref.x;
+        const int cl = side ? rec.ref.w : rec.ref.z;
+        float lo[3], hi[3];
+        child_box<D>(rec, side, lo, hi);
+        lbs[side] = box_lb2<D>(q, lo, hi);
+        // leaves are always skipped when they are in the query's component (mst.py:276);
+        // internal subtrees only under subtree skipping (mst.py:291)
+        const bool same = cl == comp && (c < 0 || kSkip);
+        want[side] = !same && lbs[side] <= r2;
+        if (want[side] && c < 0) {
+          want[side] = false;
+          ++evals;
+          const double w = exact_dist<D>(q, lo);
+          if (w <= radius) {
+            const unsigned p = __ldg(perm + (~c));
+            const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
+            const unsigned long long uv = (u << 32) | v;
+            const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
+            if (key_less(wb, uv, best_w, best_uv)) {
+              best_w = wb;
+              best_uv = uv;
+              if (w < radius) {
+                radius = w;
+                r2 = prune_r2(w);
+                if (kBounds) atomicMin(&ub[comp], wb);
+              }
             }
           }
         }
       }
-    }
-    if (want[0] && want[1]) {
-      // continue with the nearer child (ties: left), park the other
-      const int near = lbs[1] < lbs[0] ? 1 : 0;
-      if (top + 1 > kStackCapacity) {
+      const int np = (int)want[0] + (int)want[1];
+      if (top + np > kStackCapacity) {
         atomicOr(overflow, 1);
         top = 0;
-        cur = -1;
-      } else {
+      } else if (np == 2) {
+        // nearer child on top (popped first); ties keep the left child there
+        const int near = lbs[1] < lbs[0] ? 1 : 0;
         stack_node[top] = near ? rec.ref.x : rec.ref.y;
         stack_lb[top] = lbs[1 - near];
+        stack_node[top + 1] = near ? rec.ref.y : rec.ref.x;
+        stack_lb[top + 1] = lbs[near];
+        top += 2;
+      } else if (np == 1) {
+        stack_node[top] = want[0] ? rec.ref.x : rec.ref.y;
+        stack_lb[top] = want[0] ? lbs[0] : lbs[1];
         ++top;
-        cur = near ? rec.ref.y : rec.ref.x;
       }
-    } else if (want[0]) {
-      cur = rec.ref.x;
-    } else if (want[1]) {
-      cur = rec.ref.y;
-    } else {
-      cur = -1;
+    }
+    if (top == 0) {
+      if (best_uv != ~0ull) atomic_min_key(&best[comp], best_w, best_uv);
+      s = -1;
     }
   }
 #pragma unroll
