@@ -53,8 +53,8 @@ __device__ __forceinline__ bool key_less(unsigned long long w, unsigned long lon
 // only CASes while strictly smaller, so contended components rarely loop.
 __device__ __forceinline__ void atomic_min_key(EdgeKey* addr, unsigned long long w, unsigned long long uv) {
   EdgeKey cur;
-  cur.w = __ldcg(&addr->w);
-  cur.uv = __ldcg(&addr->uv);
+  // one 16-byte L2 read; a torn pair only costs one failed CAS
+  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(cur.uv), "=l"(cur.w) : "l"(addr));
   while (key_less(w, uv, cur.w, cur.uv)) {
     EdgeKey mine;
     mine.w = w;
@@ -63,6 +63,11 @@ __device__ __forceinline__ void atomic_min_key(EdgeKey* addr, unsigned long long
     if (old.w == cur.w && old.uv == cur.uv) return;
     cur = old;
   }
+}
+
+// Plain 16-byte store of a key (a component written by exactly one query).
+__device__ __forceinline__ void store_key(EdgeKey* addr, unsigned long long w, unsigned long long uv) {
+  asm volatile("st.global.v2.u64 [%0], {%1, %2};" :: "l"(addr), "l"(uv), "l"(w) : "memory");
 }
 
 // Exact reference distance: f64, axis order, correctly rounded, no FMA

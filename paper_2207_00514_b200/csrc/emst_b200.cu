@@ -78,7 +78,8 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
-  int traversal = 2;   // EMST_TRAVERSAL: 0 lane (binary), 1 packet (binary), 2 wide4, 3 wide8
+  bool singleton_round = false;   // every component is one point (round 1 of a solve)
+  int traversal = 0;   // EMST_TRAVERSAL: 0 lane (binary), 1 packet (binary), 2 wide4, 3 wide8
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
@@ -447,7 +448,7 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
     launch(c, kernel, grid, kTraverseThreads, 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p),
            (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
-           reinterpret_cast<int*>(dev_counter(c, 3)), work);
+           reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1);
   }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
@@ -570,7 +571,9 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     CK(cudaMemsetAsync(c->best.p, 0xff, comps * sizeof(EdgeKey), c->stream));
     round_prepare(c, n, bounds, &ms_labels, &ms_bounds);
     CK(cudaEventRecord(c->ev_a, c->stream));
+    c->singleton_round = comps == n;
     round_find(c, n, comps, flags);
+    c->singleton_round = false;
     CK(cudaEventRecord(c->ev_b, c->stream));
     long long emitted = 0;
     long long next = round_merge(c, n, comps, edges, &emitted);
@@ -651,7 +654,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     c = new emst_context();
     c->device = device;
     if (const char* t = getenv("EMST_TRAVERSAL"))
-      c->traversal = !strcmp(t, "lane") ? 0 : !strcmp(t, "packet") ? 1 : !strcmp(t, "wide8") ? 3 : 2;
+      c->traversal = !strcmp(t, "wide4") ? 2 : !strcmp(t, "packet") ? 1 : !strcmp(t, "wide8") ? 3 : 0;
     c->rank = rank;
     c->world = world;
     set_device(c);

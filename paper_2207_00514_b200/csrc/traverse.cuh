@@ -72,7 +72,7 @@ constexpr int kTraverseThreads = 256;
 #define EMST_TRAV_MINB 4
 #endif
 #ifndef EMST_REFILL_IDLE
-#define EMST_REFILL_IDLE 8
+#define EMST_REFILL_IDLE 16
 #endif
 constexpr int kTraverseChunk = 128;     // consecutive Morton queries a warp claims at once
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
@@ -84,7 +84,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
-           unsigned long long* __restrict__ work_counter) {
+           unsigned long long* __restrict__ work_counter, bool singletons) {
   const unsigned lane = lane_id();
   const unsigned lt = lanemask_lt_u32();
   const long long total = q1 - q0;
@@ -107,11 +107,20 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   int top = 0;
   int since_refresh = 0;
   unsigned long long evals = 0;
+  // a finished query's result waits here until the warp refills, so the
+  // L2-latency CAS of many lanes overlaps instead of stalling the warp per lane
+  bool pend = false;
+  int pcomp = 0;
+  unsigned long long pw = 0, puv = 0;
 
   for (;;) {
     // ---- refill idle lanes from the warp's chunk of consecutive Morton slots
     const unsigned idle = __ballot_sync(0xffffffffu, s < 0);
     const int n_idle = __popc(idle);
+    if (pend && (n_idle >= kRefillIdle || n_idle == 32)) {
+      atomic_min_key(&best[pcomp], pw, puv);
+      pend = false;
+    }
     if (n_idle == 32 && exhausted) break;
     if (n_idle >= kRefillIdle || n_idle == 32) {           // warp-uniform
       if (pool_next >= pool_end && !exhausted) {
@@ -213,7 +222,17 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       }
     }
     if (top == 0) {
-      if (best_uv != ~0ull) atomic_min_key(&best[comp], best_w, best_uv);
+      if (best_uv != ~0ull) {
+        if (singletons) {
+          store_key(&best[comp], best_w, best_uv);   // round 1: the query is its component
+        } else if (!(__longlong_as_double((long long)best_w) > radius)) {
+          // (a strictly smaller shared radius means another query already beat this edge)
+          pend = true;
+          pcomp = comp;
+          pw = best_w;
+          puv = best_uv;
+        }
+      }
       s = -1;
     }
   }
