@@ -72,7 +72,7 @@ constexpr int kTraverseThreads = 256;
 #define EMST_TRAV_MINB 4
 #endif
 #ifndef EMST_REFILL_IDLE
-#define EMST_REFILL_IDLE 16
+#define EMST_REFILL_IDLE 2
 #endif
 constexpr int kTraverseChunk = 128;     // consecutive Morton queries a warp claims at once
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
@@ -92,6 +92,15 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
 #pragma unroll
   for (int k = 0; k < 3; ++k) { rlo[k] = root_box->lo[k]; rhi[k] = root_box->hi[k]; }
 
+  // The warp claims kTraverseChunk consecutive Morton slots at a time and stages
+  // their point, label and starting radius in shared memory with coalesced loads,
+  // so handing a new query to an idle lane costs a few shared loads, not an
+  // L2/DRAM round trip that would stall the whole warp.
+  __shared__ float4 s_pts[kTraverseThreads / 32][kTraverseChunk];
+  __shared__ int s_lab[kTraverseThreads / 32][kTraverseChunk];
+  __shared__ unsigned long long s_ub[kTraverseThreads / 32][kTraverseChunk];
+  const int wib = threadIdx.x >> 5;
+  long long chunk_base = 0;
   long long pool_next = 0, pool_end = 0;   // warp-uniform chunk of claimed queries
   bool exhausted = false;                  // warp-uniform: global work is gone
 
@@ -114,15 +123,18 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   unsigned long long pw = 0, puv = 0;
 
   for (;;) {
-    // ---- refill idle lanes from the warp's chunk of consecutive Morton slots
+    // ---- refill idle lanes from the warp's staged chunk of consecutive Morton slots
     const unsigned idle = __ballot_sync(0xffffffffu, s < 0);
     const int n_idle = __popc(idle);
-    if (pend && (n_idle >= kRefillIdle || n_idle == 32)) {
-      atomic_min_key(&best[pcomp], pw, puv);
-      pend = false;
+    if (n_idle == 32 && exhausted) {
+      if (pend) atomic_min_key(&best[pcomp], pw, puv);
+      break;
     }
-    if (n_idle == 32 && exhausted) break;
-    if (n_idle >= kRefillIdle || n_idle == 32) {           // warp-uniform
+    if (n_idle >= kRefillIdle) {           // warp-uniform
+      if (pend) {
+        atomic_min_key(&best[pcomp], pw, puv);
+        pend = false;
+      }
       if (pool_next >= pool_end && !exhausted) {
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(work_counter, (unsigned long long)kTraverseChunk);
@@ -130,8 +142,27 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         if ((long long)base >= total) {
           exhausted = true;
         } else {
-          pool_next = (long long)base;
-          pool_end = min((long long)base + kTraverseChunk, total);
+          chunk_base = (long long)base;
+          pool_next = chunk_base;
+          pool_end = min(chunk_base + kTraverseChunk, total);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < kTraverseChunk / 32; ++j) {
+            const long long i = chunk_base + j * 32 + lane;
+            if (i < pool_end) {
+              s_pts[wib][j * 32 + lane] = spts[q0 + i];
+              s_lab[wib][j * 32 + lane] = label[q0 + i];
+            }
+          }
+          if (kBounds) {
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < kTraverseChunk / 32; ++j) {
+              const long long i = chunk_base + j * 32 + lane;
+              if (i < pool_end) s_ub[wib][j * 32 + lane] = __ldcg(&ub[s_lab[wib][j * 32 + lane]]);
+            }
+          }
+          __syncwarp();
         }
       }
       if (pool_next < pool_end) {
@@ -141,19 +172,19 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         pool_next = min(pool_end, pool_next + (long long)n_idle);
         if (take) {
           s = mine;
-          const long long slot = q0 + s;
-          const float4 qv = spts[slot];
+          const int k = (int)(mine - chunk_base);
+          const float4 qv = s_pts[wib][k];
           q[0] = qv.x; q[1] = qv.y; q[2] = qv.z;
           qp = __float_as_uint(qv.w);
-          comp = label[slot];
-          radius = kBounds ? bits_to_radius(__ldcg(&ub[comp])) : __longlong_as_double(0x7ff0000000000000ll);
+          comp = s_lab[wib][k];
+          radius = kBounds ? bits_to_radius(s_ub[wib][k]) : __longlong_as_double(0x7ff0000000000000ll);
           r2 = prune_r2(radius);
           best_w = ~0ull;
           best_uv = ~0ull;
           stack_node[0] = 0;
           stack_lb[0] = box_lb2<D>(q, rlo, rhi);
           top = 1;
-          since_refresh = 0;
+          since_refresh = kRadiusRefresh / 2;   // staged radius may be stale: refresh early
         }
       }
     }
