@@ -79,6 +79,8 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
   bool singleton_round = false;   // every component is one point (round 1 of a solve)
+  int round = 0;                  // 1-based Boruvka round of the running solve (0 outside)
+  int packet_from = 1 << 30;      // rounds >= this use the warp-packet traversal (EMST_PACKET_FROM)
   int traversal = 0;   // EMST_TRAVERSAL: 0 lane (binary), 1 packet (binary), 2 wide4, 3 wide8
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
@@ -439,7 +441,7 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
              (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
              reinterpret_cast<int*>(dev_counter(c, 3)), work);
     }
-  } else if (c->traversal == 1) {
+  } else if (c->traversal == 1 || c->round >= c->packet_from) {
     launch(c, k_traverse_packet<D, S, B>, grid_for(q1 - q0, kTraverseThreads), kTraverseThreads, 0,
            (const Node*)reinterpret_cast<Node*>(c->nodes.p), (const float4*)c->spts.p, (const unsigned*)c->perm.p,
            (const int*)c->label.p, c->ub.p, out, q0, q1, (const Box3*)c->root_box.p,
@@ -572,8 +574,10 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     round_prepare(c, n, bounds, &ms_labels, &ms_bounds);
     CK(cudaEventRecord(c->ev_a, c->stream));
     c->singleton_round = comps == n;
+    c->round = st->iterations;
     round_find(c, n, comps, flags);
     c->singleton_round = false;
+    c->round = 0;
     CK(cudaEventRecord(c->ev_b, c->stream));
     long long emitted = 0;
     long long next = round_merge(c, n, comps, edges, &emitted);
@@ -653,6 +657,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (world < 1 || rank < 0 || rank >= world) fail(EMST_ERR_PARAM, "bad rank %d / world %d", rank, world);
     c = new emst_context();
     c->device = device;
+    if (const char* t = getenv("EMST_PACKET_FROM")) c->packet_from = atoi(t);
     if (const char* t = getenv("EMST_TRAVERSAL"))
       c->traversal = !strcmp(t, "wide4") ? 2 : !strcmp(t, "packet") ? 1 : !strcmp(t, "wide8") ? 3 : 0;
     c->rank = rank;

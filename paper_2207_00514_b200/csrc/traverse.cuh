@@ -72,7 +72,7 @@ constexpr int kTraverseThreads = 256;
 #define EMST_TRAV_MINB 4
 #endif
 #ifndef EMST_REFILL_IDLE
-#define EMST_REFILL_IDLE 2
+#define EMST_REFILL_IDLE 16
 #endif
 constexpr int kTraverseChunk = 128;     // consecutive Morton queries a warp claims at once
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
