@@ -76,6 +76,9 @@ typedef struct emst_stats {
   double traverse_ms;           /* device time of the traversal kernel launches */
   int64_t traverse_launches;
   int64_t traverse_queries;     /* queries those launches processed (this rank) */
+  double round_traverse_ms[64]; /* per Boruvka round: traversal device time */
+  int64_t round_node_visits[64];/* per round: node records fetched by the traversal */
+  int64_t round_found[64];      /* per round: queries that found a candidate edge */
 } emst_stats;
 
 typedef struct emst_context emst_context;

@@ -72,6 +72,9 @@ class Stats(ctypes.Structure):
         ("traverse_ms", ctypes.c_double),
         ("traverse_launches", ctypes.c_int64),
         ("traverse_queries", ctypes.c_int64),
+        ("round_traverse_ms", ctypes.c_double * 64),
+        ("round_node_visits", ctypes.c_int64 * 64),
+        ("round_found", ctypes.c_int64 * 64),
     ]
 
 

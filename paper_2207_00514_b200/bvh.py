@@ -82,7 +82,13 @@ def _device_points(points):
             return points.data_ptr(), n, d, _lib.POINTS_ON_DEVICE, points
     except ImportError:
         pass
-    pts = as_point_array(points)
+    arr = np.asarray(points)
+    if arr.dtype == np.float32 and arr.ndim == 2 and arr.flags.c_contiguous:
+        # already in the device layout: the finiteness check (and the reference's
+        # "point {row} has a non-finite coordinate" error) runs on the GPU in k_scene
+        n, d = check_shape(arr)
+        return arr.ctypes.data, n, d, 0, arr
+    pts = as_point_array(arr)
     n, d = pts.shape
     return pts.ctypes.data, n, d, 0, pts
 

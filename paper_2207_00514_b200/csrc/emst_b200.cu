@@ -565,6 +565,8 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   st->component_counts[0] = n;
   st->num_counts = 1;
   double ms_labels = 0, ms_bounds = 0, ms_find = 0, ms_merge = 0;
+  long long visits_before = 0, found_before = 0;
+  double tv_before = c->traverse_ms;
   const bool bounds = flags & EMST_UPPER_BOUNDS;
   while (comps > 1) {
     st->iterations++;
@@ -581,6 +583,15 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     CK(cudaEventRecord(c->ev_b, c->stream));
     long long emitted = 0;
     long long next = round_merge(c, n, comps, edges, &emitted);
+    if (st->iterations <= 64) {
+      const int r = st->iterations - 1;
+      st->round_traverse_ms[r] = c->traverse_ms - tv_before;
+      st->round_node_visits[r] = c->host_counters[5] - visits_before;
+      st->round_found[r] = c->host_counters[6] - found_before;
+      visits_before = c->host_counters[5];
+      found_before = c->host_counters[6];
+      tv_before = c->traverse_ms;
+    }
     float a = 0.f;
     CK(cudaEventElapsedTime(&a, c->ev_a, c->ev_b));
     ms_find += a;

@@ -121,6 +121,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   bool pend = false;
   int pcomp = 0;
   unsigned long long pw = 0, puv = 0;
+  unsigned long long visits = 0, found = 0;
 
   for (;;) {
     // ---- refill idle lanes from the warp's staged chunk of consecutive Morton slots
@@ -199,6 +200,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       if (shared < radius) { radius = shared; r2 = prune_r2(shared); }
     }
     if (plb <= r2) {
+      ++visits;
       const auto rec = load_node(nodes + stack_node[top]);
       float lbs[2];
       bool want[2];
@@ -254,6 +256,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     }
     if (top == 0) {
       if (best_uv != ~0ull) {
+        ++found;
         if (singletons) {
           store_key(&best[comp], best_w, best_uv);   // round 1: the query is its component
         } else if (!(__longlong_as_double((long long)best_w) > radius)) {
@@ -268,8 +271,16 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
-  if (lane == 0 && evals) atomicAdd(evals_out, evals);
+  for (int o = 16; o > 0; o >>= 1) {
+    evals += __shfl_xor_sync(0xffffffffu, evals, o);
+    visits += __shfl_xor_sync(0xffffffffu, visits, o);
+    found += __shfl_xor_sync(0xffffffffu, found, o);
+  }
+  if (lane == 0) {
+    if (evals) atomicAdd(evals_out, evals);
+    if (visits) atomicAdd(evals_out + 5, visits);   // counters[5]: node visits
+    if (found) atomicAdd(evals_out + 6, found);     // counters[6]: queries with a candidate
+  }
 }
 
 
