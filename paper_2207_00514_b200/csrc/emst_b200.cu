@@ -113,6 +113,7 @@ struct emst_context {
   int wide_w = 0;                 // children per wide node (0: no wide tree)
   // rounds
   DevBuf<int> label, bprefix;
+  DevBuf<float> nfn_lb;   // per slot: proven lower bound on the nearest-foreign distance
   DevBuf<unsigned long long> ub;
   DevBuf<EdgeKey> best, shard_keys;
   DevBuf<int> succ, ptr, root, newid, fin;
@@ -345,6 +346,7 @@ void check_shape(long long n, int d) {
 void ensure_rounds(emst_context* c, long long n) {
   c->label.ensure(n);
   c->bprefix.ensure(n);
+  c->nfn_lb.ensure(n);
   c->ub.ensure(n);
   c->best.ensure(n);
   c->succ.ensure(n);
@@ -450,7 +452,8 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
     launch(c, kernel, grid, kTraverseThreads, 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p),
            (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
-           reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1);
+           reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1,
+           c->nfn_lb.p);
   }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
@@ -560,6 +563,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   ensure_rounds(c, n);
   CK(cudaMemsetAsync(c->counters.p, 0, 8 * sizeof(long long), c->stream));
   launch(c, k_iota_int, grid_for(n, 256), 256, 0, c->label.p, n);
+  CK(cudaMemsetAsync(c->nfn_lb.p, 0, n * sizeof(float), c->stream));
   long long comps = n, edges = 0;
   const int max_it = max_iterations(n);
   st->component_counts[0] = n;
@@ -708,7 +712,7 @@ int emst_context_destroy(emst_context* c) {
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
   c->node_parent.release(); c->leaf_parent.release(); c->arrivals.release(); c->root_box.release();
   c->wnodes.release(); c->wrange.release(); c->wtmp.release();
-  c->label.release(); c->bprefix.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
+  c->label.release(); c->bprefix.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->eu.release(); c->ev.release(); c->ew.release(); c->xw.release(); c->xuv.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release();
@@ -920,6 +924,7 @@ void prepare_labels_from_host(emst_context* c, const int64_t* labels, long long 
   lab.ensure(n);
   CK(cudaMemcpyAsync(lab.p, labels, n * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
   launch(c, k_labels_to_slots, grid_for(n, 256), 256, 0, (const long long*)lab.p, (const unsigned*)c->perm.p, n, c->label.p);
+  CK(cudaMemsetAsync(c->nfn_lb.p, 0, n * sizeof(float), c->stream));
   CK(cudaStreamSynchronize(c->stream));
   lab.release();
 }

@@ -84,7 +84,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
-           unsigned long long* __restrict__ work_counter, bool singletons) {
+           unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb) {
   const unsigned lane = lane_id();
   const unsigned lt = lanemask_lt_u32();
   const long long total = q1 - q0;
@@ -99,6 +99,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   __shared__ float4 s_pts[kTraverseThreads / 32][kTraverseChunk];
   __shared__ int s_lab[kTraverseThreads / 32][kTraverseChunk];
   __shared__ unsigned long long s_ub[kTraverseThreads / 32][kTraverseChunk];
+  __shared__ float s_nlb[kTraverseThreads / 32][kTraverseChunk];
   const int wib = threadIdx.x >> 5;
   long long chunk_base = 0;
   long long pool_next = 0, pool_end = 0;   // warp-uniform chunk of claimed queries
@@ -153,6 +154,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
             if (i < pool_end) {
               s_pts[wib][j * 32 + lane] = spts[q0 + i];
               s_lab[wib][j * 32 + lane] = label[q0 + i];
+              if (kBounds) s_nlb[wib][j * 32 + lane] = nfn_lb[q0 + i];
             }
           }
           if (kBounds) {
@@ -186,6 +188,10 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           stack_lb[0] = box_lb2<D>(q, rlo, rhi);
           top = 1;
           since_refresh = kRadiusRefresh / 2;   // staged radius may be stale: refresh early
+          // A previous round proved every foreign point is farther than nfn_lb[s]
+          // (foreign sets only shrink, so that stays true).  If that already
+          // exceeds the radius, this query cannot find an edge: done.
+          if (kBounds && (double)s_nlb[wib][k] > radius) top = 0;
         }
       }
     }
@@ -255,6 +261,12 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       }
     }
     if (top == 0) {
+      // the search just proved: no foreign point closer than the final radius
+      if (kBounds) {
+        const float proven = __double2float_rd(radius);
+        const long long slot = q0 + s;
+        if (proven > nfn_lb[slot]) nfn_lb[slot] = proven;
+      }
       if (best_uv != ~0ull) {
         ++found;
         if (singletons) {
