@@ -191,7 +191,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           // A previous round proved every foreign point is farther than nfn_lb[s]
           // (foreign sets only shrink, so that stays true).  If that already
           // exceeds the radius, this query cannot find an edge: done.
-          if (kBounds && (double)s_nlb[wib][k] > radius) top = 0;
+          if (kBounds && (double)s_nlb[wib][k] > radius) r2 = -1.f;   // root gets pruned at once
         }
       }
     }
