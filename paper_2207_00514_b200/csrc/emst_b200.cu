@@ -81,6 +81,7 @@ struct emst_context {
   bool singleton_round = false;   // every component is one point (round 1 of a solve)
   int round = 0;                  // 1-based Boruvka round of the running solve (0 outside)
   int packet_from = 1 << 30;      // rounds >= this use the warp-packet traversal (EMST_PACKET_FROM)
+  bool two_pass = true;           // EMST_TWO_PASS=0 disables the boundary-first split
   int traversal = 0;   // EMST_TRAVERSAL: 0 lane (binary), 1 packet (binary), 2 wide4, 3 wide8
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
@@ -412,7 +413,22 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
 }
 
 template <int D, bool S, bool B>
+void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1, int pass);
+
+template <int D, bool S, bool B>
 void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
+  // boundary queries first (pass 1), then the rest (pass 2); round 1 and runs
+  // without radius seeding have nothing to gain from the split
+  if (B && !c->singleton_round && c->two_pass) {
+    traverse_range<D, S, B>(c, out, q0, q1, 1);
+    traverse_range<D, S, B>(c, out, q0, q1, 2);
+  } else {
+    traverse_range<D, S, B>(c, out, q0, q1, 0);
+  }
+}
+
+template <int D, bool S, bool B>
+void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1, int pass) {
   if (q1 <= q0) return;
   using Node = typename NodeOf<D>::type;
   auto kernel = k_traverse<D, S, B>;
@@ -453,7 +469,7 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
            (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
            reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1,
-           c->nfn_lb.p);
+           c->nfn_lb.p, (const int*)c->bprefix.p, c->n, pass);
   }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
@@ -673,6 +689,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     c = new emst_context();
     c->device = device;
     if (const char* t = getenv("EMST_PACKET_FROM")) c->packet_from = atoi(t);
+    if (const char* t = getenv("EMST_TWO_PASS")) c->two_pass = atoi(t) != 0;
     if (const char* t = getenv("EMST_TRAVERSAL"))
       c->traversal = !strcmp(t, "wide4") ? 2 : !strcmp(t, "packet") ? 1 : !strcmp(t, "wide8") ? 3 : 0;
     c->rank = rank;

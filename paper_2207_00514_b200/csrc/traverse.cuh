@@ -84,7 +84,8 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
-           unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb) {
+           unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb,
+           const int* __restrict__ bprefix, long long n, int pass) {
   const unsigned lane = lane_id();
   const unsigned lt = lanemask_lt_u32();
   const long long total = q1 - q0;
@@ -100,6 +101,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   __shared__ int s_lab[kTraverseThreads / 32][kTraverseChunk];
   __shared__ unsigned long long s_ub[kTraverseThreads / 32][kTraverseChunk];
   __shared__ float s_nlb[kTraverseThreads / 32][kTraverseChunk];
+  __shared__ bool s_run[kTraverseThreads / 32][kTraverseChunk];
   const int wib = threadIdx.x >> 5;
   long long chunk_base = 0;
   long long pool_next = 0, pool_end = 0;   // warp-uniform chunk of claimed queries
@@ -155,6 +157,17 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
               s_pts[wib][j * 32 + lane] = spts[q0 + i];
               s_lab[wib][j * 32 + lane] = label[q0 + i];
               if (kBounds) s_nlb[wib][j * 32 + lane] = nfn_lb[q0 + i];
+              bool run = true;
+              if (pass != 0) {
+                // pass 1: slots with a Z-order neighbour in another component (the
+                // likely endpoints of component minima, run first so the shared
+                // radii are tight); pass 2: everything else
+                const long long g = q0 + i;
+                const int b = bprefix[g];
+                const bool bnd = (g + 1 < n && bprefix[g + 1] != b) || (g > 0 && bprefix[g - 1] != b);
+                run = (pass == 1) == bnd;
+              }
+              s_run[wib][j * 32 + lane] = run;
             }
           }
           if (kBounds) {
@@ -192,6 +205,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           // (foreign sets only shrink, so that stays true).  If that already
           // exceeds the radius, this query cannot find an edge: done.
           if (kBounds && (double)s_nlb[wib][k] > radius) r2 = -1.f;   // root gets pruned at once
+          if (!s_run[wib][k]) { r2 = -1.f; radius = -1.0; }        // not this pass: no work, no bound update
         }
       }
     }
@@ -262,7 +276,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     }
     if (top == 0) {
       // the search just proved: no foreign point closer than the final radius
-      if (kBounds) {
+      if (kBounds && radius >= 0.0) {
         const float proven = __double2float_rd(radius);
         const long long slot = q0 + s;
         if (proven > nfn_lb[slot]) nfn_lb[slot] = proven;
