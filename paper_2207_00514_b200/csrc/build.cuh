@@ -16,16 +16,6 @@
 
 namespace emst {
 
-struct Scene {
-  double lo[3];
-  double inv[3];
-  float flo[3];
-  float fhi[3];
-  long long bad_row;     // first row holding a non-finite coordinate, or LLONG_MAX
-  unsigned blocks_done;
-  int pad;
-};
-
 constexpr int kSceneThreads = 256;
 
 template <int D>
@@ -105,36 +95,6 @@ k_scene(const float* __restrict__ pts, long long n, float* __restrict__ part_lo,
   scene->blocks_done = 0;
 }
 
-// Spread the low bits of v so consecutive bits land D positions apart.
-__device__ __forceinline__ unsigned long long spread_bits3(unsigned long long v) {
-  v &= 0x1fffffull;
-  v = (v | (v << 32)) & 0x001f00000000ffffull;
-  v = (v | (v << 16)) & 0x001f0000ff0000ffull;
-  v = (v | (v << 8)) & 0x100f00f00f00f00full;
-  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
-  v = (v | (v << 2)) & 0x1249249249249249ull;
-  return v;
-}
-__device__ __forceinline__ unsigned long long spread_bits2(unsigned long long v) {
-  v &= 0x7fffffffull;
-  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
-  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
-  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
-  v = (v | (v << 2)) & 0x3333333333333333ull;
-  v = (v | (v << 1)) & 0x5555555555555555ull;
-  return v;
-}
-
-// Lattice cell of one coordinate (geometry.py:169-177): f64 (x - lo) * inv,
-// clamped to [0, nextafter(1, 0)], scaled by 2^bits and truncated.
-__device__ __forceinline__ unsigned long long lattice_cell(float x, double lo, double inv, double scale) {
-  double t = __dmul_rn(__dsub_rn((double)x, lo), inv);
-  const double below_one = 0x1.fffffffffffffp-1;
-  if (t < 0.0) t = 0.0;
-  else if (t > below_one) t = below_one;
-  return __double2ull_rz(__dmul_rn(t, scale));
-}
-
 template <int D>
 __global__ void k_morton(const float* __restrict__ pts, long long n, const Scene* __restrict__ scene,
                          unsigned long long* __restrict__ codes) {
@@ -182,7 +142,8 @@ __device__ __forceinline__ int leaf_ref(long long s) { return ~(int)s; }
 
 template <class Node>
 __global__ void k_karras(const unsigned long long* __restrict__ sc, long long n, Node* __restrict__ nodes,
-                         int2* __restrict__ range, int* __restrict__ node_parent, int* __restrict__ leaf_parent) {
+                         int2* __restrict__ range, int* __restrict__ node_parent, int* __restrict__ leaf_parent,
+                         int* __restrict__ node_delta) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long m = n - 1;
   if (i >= m) return;
@@ -209,6 +170,15 @@ __global__ void k_karras(const unsigned long long* __restrict__ sc, long long n,
   else { rref = (int)(gamma + 1); node_parent[gamma + 1] = (int)((i << 1) | 1); }
   nodes[i].ref = make_int4(lref, rref, kMixed, kMixed);
   range[i] = make_int2((int)lo, (int)hi);
+  node_delta[i] = node_len;
+  if (i == 0) node_parent[0] = -1;
+}
+
+// (parent link, prefix length) per internal node: one 8-byte load per climb step
+__global__ void k_pack_up(const int* __restrict__ node_parent, const int* __restrict__ node_delta, long long m,
+                          int2* __restrict__ up) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < m) up[i] = make_int2(node_parent[i], node_delta[i]);
 }
 
 // --- child box slots inside a node record

@@ -113,4 +113,74 @@ __device__ __forceinline__ double bits_to_radius(unsigned long long b) {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+struct Scene {
+  double lo[3];
+  double inv[3];
+  float flo[3];
+  float fhi[3];
+  long long bad_row;     // first row holding a non-finite coordinate, or LLONG_MAX
+  unsigned blocks_done;
+  int pad;
+};
+
+// Spread the low bits of v so consecutive bits land D positions apart.
+__device__ __forceinline__ unsigned long long spread_bits3(unsigned long long v) {
+  v &= 0x1fffffull;
+  v = (v | (v << 32)) & 0x001f00000000ffffull;
+  v = (v | (v << 16)) & 0x001f0000ff0000ffull;
+  v = (v | (v << 8)) & 0x100f00f00f00f00full;
+  v = (v | (v << 4)) & 0x10c30c30c30c30c3ull;
+  v = (v | (v << 2)) & 0x1249249249249249ull;
+  return v;
+}
+__device__ __forceinline__ unsigned long long spread_bits2(unsigned long long v) {
+  v &= 0x7fffffffull;
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+// Lattice cell of one coordinate (geometry.py:169-177): f64 (x - lo) * inv,
+// clamped to [0, nextafter(1, 0)], scaled by 2^bits and truncated.  Monotone
+// non-decreasing in x (every step is a correctly rounded monotone operation).
+__device__ __forceinline__ unsigned long long lattice_cell_d(double x, double lo, double inv, double scale) {
+  double t = __dmul_rn(__dsub_rn(x, lo), inv);
+  const double below_one = 0x1.fffffffffffffp-1;
+  if (t < 0.0) t = 0.0;
+  else if (t > below_one) t = below_one;
+  return __double2ull_rz(__dmul_rn(t, scale));
+}
+__device__ __forceinline__ unsigned long long lattice_cell(float x, double lo, double inv, double scale) {
+  return lattice_cell_d((double)x, lo, inv, scale);
+}
+
+// Morton code of a lattice cell triple (x most significant), as in k_morton.
+template <int D>
+__device__ __forceinline__ unsigned long long morton_of_cells(const unsigned long long* c) {
+  if (D == 3) return (spread_bits3(c[0]) << 2) | (spread_bits3(c[1]) << 1) | spread_bits3(c[2]);
+  return (spread_bits2(c[0]) << 1) | spread_bits2(c[1]);
+}
+
+// Length of the Morton prefix shared by every lattice cell the box
+// [q - r, q + r] can touch.  The quantiser is monotone per axis, so all points
+// inside the box have codes between the codes of its two corners; corners are
+// rounded outward and r is inflated past any f64 rounding of a distance, so a
+// point whose distance evaluates to <= r cannot fall outside.
+template <int D>
+__device__ __forceinline__ int ball_prefix(const float* q, double r, const Scene& sc) {
+  const double scale = D == 3 ? 2097152.0 : 2147483648.0;
+  const double rr = __dmul_ru(r, 1.0 + 0x1p-40);
+  unsigned long long clo[3], chi[3];
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    clo[k] = lattice_cell_d(__dsub_rd((double)q[k], rr), sc.lo[k], sc.inv[k], scale);
+    chi[k] = lattice_cell_d(__dadd_ru((double)q[k], rr), sc.lo[k], sc.inv[k], scale);
+  }
+  const unsigned long long a = morton_of_cells<D>(clo), b = morton_of_cells<D>(chi);
+  return a == b ? 64 : __clzll((long long)(a ^ b));
+}
+
 }  // namespace emst

@@ -81,7 +81,6 @@ struct emst_context {
   bool singleton_round = false;   // every component is one point (round 1 of a solve)
   int round = 0;                  // 1-based Boruvka round of the running solve (0 outside)
   int packet_from = 1 << 30;      // rounds >= this use the warp-packet traversal (EMST_PACKET_FROM)
-  bool two_pass = true;           // EMST_TWO_PASS=0 disables the boundary-first split
   int traversal = 0;   // EMST_TRAVERSAL: 0 lane (binary), 1 packet (binary), 2 wide4, 3 wide8
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
@@ -104,7 +103,8 @@ struct emst_context {
   DevBuf<unsigned> perm, iperm;
   DevBuf<unsigned char> nodes;   // Node2 / Node3 records
   DevBuf<int2> range;
-  DevBuf<int> node_parent, leaf_parent;
+  DevBuf<int> node_parent, leaf_parent, node_delta;
+  DevBuf<int2> up;   // (parent link, prefix length) per internal node
   DevBuf<unsigned> arrivals;
   DevBuf<Box3> root_box;
   DevBuf<unsigned char> wnodes;   // wide traversal tree (WideNode<D, W>)
@@ -238,6 +238,8 @@ void ensure_build(emst_context* c, long long n, int d) {
   c->range.ensure(std::max<long long>(n - 1, 1));
   c->node_parent.ensure(std::max<long long>(n - 1, 1));
   c->leaf_parent.ensure(n);
+  c->node_delta.ensure(std::max<long long>(n - 1, 1));
+  c->up.ensure(std::max<long long>(n - 1, 1));
   c->arrivals.ensure(std::max<long long>(n - 1, 1));
   c->root_box.ensure(1);
   c->counters.ensure(8);
@@ -313,17 +315,20 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
     if (d == 3) {
       Node3* nodes = reinterpret_cast<Node3*>(c->nodes.p);
       launch(c, k_karras<Node3>, grid_for(m, 256), 256, 0, (const unsigned long long*)skeys, n, nodes, c->range.p,
-             c->node_parent.p, c->leaf_parent.p);
+             c->node_parent.p, c->leaf_parent.p, c->node_delta.p);
       launch(c, k_refit<Node3>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, nodes,
              (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p);
     } else {
       Node2* nodes = reinterpret_cast<Node2*>(c->nodes.p);
       launch(c, k_karras<Node2>, grid_for(m, 256), 256, 0, (const unsigned long long*)skeys, n, nodes, c->range.p,
-             c->node_parent.p, c->leaf_parent.p);
+             c->node_parent.p, c->leaf_parent.p, c->node_delta.p);
       launch(c, k_refit<Node2>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, nodes,
              (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p);
     }
   }
+  if (n > 1)
+    launch(c, k_pack_up, grid_for(n - 1, 256), 256, 0, (const int*)c->node_parent.p, (const int*)c->node_delta.p, n - 1,
+           c->up.p);
   c->tree_valid = true;
   c->wide_w = 0;
   if (n > 1 && c->traversal >= 2) build_wide(c, n, d, c->traversal == 3 ? 3 : 2);
@@ -413,22 +418,7 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
 }
 
 template <int D, bool S, bool B>
-void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1, int pass);
-
-template <int D, bool S, bool B>
 void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
-  // boundary queries first (pass 1), then the rest (pass 2); round 1 and runs
-  // without radius seeding have nothing to gain from the split
-  if (B && !c->singleton_round && c->two_pass) {
-    traverse_range<D, S, B>(c, out, q0, q1, 1);
-    traverse_range<D, S, B>(c, out, q0, q1, 2);
-  } else {
-    traverse_range<D, S, B>(c, out, q0, q1, 0);
-  }
-}
-
-template <int D, bool S, bool B>
-void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1, int pass) {
   if (q1 <= q0) return;
   using Node = typename NodeOf<D>::type;
   auto kernel = k_traverse<D, S, B>;
@@ -469,7 +459,7 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1, i
            (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
            reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1,
-           c->nfn_lb.p, (const int*)c->bprefix.p, c->n, pass);
+           c->nfn_lb.p, (const int2*)c->up.p, (const int*)c->leaf_parent.p, (const Scene*)c->scene.p);
   }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
@@ -689,7 +679,6 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     c = new emst_context();
     c->device = device;
     if (const char* t = getenv("EMST_PACKET_FROM")) c->packet_from = atoi(t);
-    if (const char* t = getenv("EMST_TWO_PASS")) c->two_pass = atoi(t) != 0;
     if (const char* t = getenv("EMST_TRAVERSAL"))
       c->traversal = !strcmp(t, "wide4") ? 2 : !strcmp(t, "packet") ? 1 : !strcmp(t, "wide8") ? 3 : 0;
     c->rank = rank;
@@ -727,7 +716,7 @@ int emst_context_destroy(emst_context* c) {
   c->k0.release(); c->k1.release(); c->v0.release(); c->v1.release();
   c->sort_hist.release(); c->sort_off.release(); c->sort_status.release(); c->sort_misc.release();
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
-  c->node_parent.release(); c->leaf_parent.release(); c->arrivals.release(); c->root_box.release();
+  c->node_parent.release(); c->leaf_parent.release(); c->node_delta.release(); c->up.release(); c->arrivals.release(); c->root_box.release();
   c->wnodes.release(); c->wrange.release(); c->wtmp.release();
   c->label.release(); c->bprefix.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();

@@ -78,6 +78,53 @@ constexpr int kTraverseChunk = 128;     // consecutive Morton queries a warp cla
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
 constexpr int kRadiusRefresh = 16;      // pops between re-reads of the shared radius
 
+// Visit one child of a fetched node record: the f32 lower bound, the component
+// skip (leaves always, mst.py:276; subtrees under subtree_skip, mst.py:291),
+// and for a surviving leaf the exact f64 reference weight (mst.py:270-289).
+// Returns true when an internal child should be explored (lb in *lb_out).
+template <int D, bool kSkip, bool kBounds, class Rec>
+__device__ __forceinline__ bool visit_child(const Rec& rec, int side, const float* q, unsigned qp, int comp,
+                                            double& radius, float& r2, unsigned long long& best_w,
+                                            unsigned long long& best_uv, const unsigned* __restrict__ perm,
+                                            unsigned long long* ub, unsigned long long& evals, float* lb_out) {
+  const int c = side ? rec.ref.y : rec.ref.x;
+  const int cl = side ? rec.ref.w : rec.ref.z;
+  float lo[3], hi[3];
+  child_box<D>(rec, side, lo, hi);
+  const float lb = box_lb2<D>(q, lo, hi);
+  *lb_out = lb;
+  const bool same = cl == comp && (c < 0 || kSkip);
+  if (same || lb > r2) return false;
+  if (c >= 0) return true;
+  ++evals;
+  const double w = exact_dist<D>(q, lo);
+  if (w <= radius) {
+    const unsigned p = __ldg(perm + (~c));
+    const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
+    const unsigned long long uv = (u << 32) | v;
+    const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
+    if (key_less(wb, uv, best_w, best_uv)) {
+      best_w = wb;
+      best_uv = uv;
+      if (w < radius) {
+        radius = w;
+        r2 = prune_r2(w);
+        if (kBounds) atomicMin(&ub[comp], wb);
+      }
+    }
+  }
+  return false;
+}
+
+// Bottom-up ("climb") traversal.  A query starts at its own leaf and climbs the
+// Karras tree; at every ancestor it explores only the sibling subtree (top-down,
+// nearest first, with the stack), so the root-to-leaf path is never walked
+// downward.  The climb stops at the first ancestor whose Morton prefix is no
+// longer than the prefix shared by the query's whole search box [q - r, q + r]:
+// every point within r has a code with that prefix, and a Karras node holds ALL
+// points with its prefix, so nothing outside that ancestor can be within r.
+// In round 1 (radius = distance to a Z-order neighbour) this stops a few levels
+// above the leaf instead of walking ~38 levels down from the root.
 template <int D, bool kSkip, bool kBounds>
 __global__ void __launch_bounds__(kTraverseThreads, EMST_TRAV_MINB)
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
@@ -85,23 +132,20 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
            unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb,
-           const int* __restrict__ bprefix, long long n, int pass) {
+           const int2* __restrict__ up, const int* __restrict__ leaf_parent, const Scene* __restrict__ scene_ptr) {
   const unsigned lane = lane_id();
   const unsigned lt = lanemask_lt_u32();
   const long long total = q1 - q0;
-  float rlo[3], rhi[3];
-#pragma unroll
-  for (int k = 0; k < 3; ++k) { rlo[k] = root_box->lo[k]; rhi[k] = root_box->hi[k]; }
+  const Scene sc = *scene_ptr;
 
   // The warp claims kTraverseChunk consecutive Morton slots at a time and stages
-  // their point, label and starting radius in shared memory with coalesced loads,
-  // so handing a new query to an idle lane costs a few shared loads, not an
-  // L2/DRAM round trip that would stall the whole warp.
+  // their point, label, leaf parent, starting radius and proven nearest-foreign
+  // bound in shared memory with coalesced loads.
   __shared__ float4 s_pts[kTraverseThreads / 32][kTraverseChunk];
   __shared__ int s_lab[kTraverseThreads / 32][kTraverseChunk];
+  __shared__ int s_lp[kTraverseThreads / 32][kTraverseChunk];
   __shared__ unsigned long long s_ub[kTraverseThreads / 32][kTraverseChunk];
   __shared__ float s_nlb[kTraverseThreads / 32][kTraverseChunk];
-  __shared__ bool s_run[kTraverseThreads / 32][kTraverseChunk];
   const int wib = threadIdx.x >> 5;
   long long chunk_base = 0;
   long long pool_next = 0, pool_end = 0;   // warp-uniform chunk of claimed queries
@@ -117,6 +161,10 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   int stack_node[kStackCapacity];
   float stack_lb[kStackCapacity];
   int top = 0;
+  int climb = -1;          // ancestor whose sibling subtree is next, -1 = climb over
+  int path_side = 0;       // which child of `climb` the query came from
+  int prefix = 0;          // Morton prefix shared by the search box
+  double prefix_r = 0.0;   // radius `prefix` was computed for
   int since_refresh = 0;
   unsigned long long evals = 0;
   // a finished query's result waits here until the warp refills, so the
@@ -156,18 +204,8 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
             if (i < pool_end) {
               s_pts[wib][j * 32 + lane] = spts[q0 + i];
               s_lab[wib][j * 32 + lane] = label[q0 + i];
+              s_lp[wib][j * 32 + lane] = leaf_parent[q0 + i];
               if (kBounds) s_nlb[wib][j * 32 + lane] = nfn_lb[q0 + i];
-              bool run = true;
-              if (pass != 0) {
-                // pass 1: slots with a Z-order neighbour in another component (the
-                // likely endpoints of component minima, run first so the shared
-                // radii are tight); pass 2: everything else
-                const long long g = q0 + i;
-                const int b = bprefix[g];
-                const bool bnd = (g + 1 < n && bprefix[g + 1] != b) || (g > 0 && bprefix[g - 1] != b);
-                run = (pass == 1) == bnd;
-              }
-              s_run[wib][j * 32 + lane] = run;
             }
           }
           if (kBounds) {
@@ -197,86 +235,84 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           r2 = prune_r2(radius);
           best_w = ~0ull;
           best_uv = ~0ull;
-          stack_node[0] = 0;
-          stack_lb[0] = box_lb2<D>(q, rlo, rhi);
-          top = 1;
+          top = 0;
+          const int link = s_lp[wib][k];
+          climb = link >> 1;
+          path_side = link & 1;
+          prefix = radius < 1e300 ? ball_prefix<D>(q, radius, sc) : -1;
+          prefix_r = radius;
           since_refresh = kRadiusRefresh / 2;   // staged radius may be stale: refresh early
           // A previous round proved every foreign point is farther than nfn_lb[s]
           // (foreign sets only shrink, so that stays true).  If that already
           // exceeds the radius, this query cannot find an edge: done.
-          if (kBounds && (double)s_nlb[wib][k] > radius) r2 = -1.f;   // root gets pruned at once
-          if (!s_run[wib][k]) { r2 = -1.f; radius = -1.0; }        // not this pass: no work, no bound update
+          if (kBounds && (double)s_nlb[wib][k] > radius) climb = -1;
         }
       }
     }
     if (s < 0) continue;
 
-    // ---- one pop
-    --top;
-    const float plb = stack_lb[top];
     if (kBounds && ++since_refresh >= kRadiusRefresh) {
       since_refresh = 0;
       const double shared = bits_to_radius(__ldcg(&ub[comp]));
       if (shared < radius) { radius = shared; r2 = prune_r2(shared); }
     }
-    if (plb <= r2) {
-      ++visits;
-      const auto rec = load_node(nodes + stack_node[top]);
-      float lbs[2];
-      bool want[2];
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int c = side ? rec.ref.y : rec.ref.x;
-        const int cl = side ? rec.ref.w : rec.ref.z;
-        float lo[3], hi[3];
-        child_box<D>(rec, side, lo, hi);
-        lbs[side] = box_lb2<D>(q, lo, hi);
-        // leaves are always skipped when they are in the query's component (mst.py:276);
-        // internal subtrees only under subtree skipping (mst.py:291)
-        const bool same = cl == comp && (c < 0 || kSkip);
-        want[side] = !same && lbs[side] <= r2;
-        if (want[side] && c < 0) {
-          want[side] = false;
-          ++evals;
-          const double w = exact_dist<D>(q, lo);
-          if (w <= radius) {
-            const unsigned p = __ldg(perm + (~c));
-            const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
-            const unsigned long long uv = (u << 32) | v;
-            const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
-            if (key_less(wb, uv, best_w, best_uv)) {
-              best_w = wb;
-              best_uv = uv;
-              if (w < radius) {
-                radius = w;
-                r2 = prune_r2(w);
-                if (kBounds) atomicMin(&ub[comp], wb);
-              }
-            }
-          }
+    if (top > 0) {
+      // ---- explore a parked sibling subtree top-down
+      --top;
+      if (stack_lb[top] <= r2) {
+        ++visits;
+        const auto rec = load_node(nodes + stack_node[top]);
+        float lbs[2];
+        const bool w0 = visit_child<D, kSkip, kBounds>(rec, 0, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
+                                                       evals, &lbs[0]);
+        const bool w1 = visit_child<D, kSkip, kBounds>(rec, 1, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
+                                                       evals, &lbs[1]);
+        const bool want0 = w0 && lbs[0] <= r2, want1 = w1 && lbs[1] <= r2;
+        const int np = (int)want0 + (int)want1;
+        if (top + np > kStackCapacity) {
+          atomicOr(overflow, 1);
+          top = 0;
+          climb = -1;
+        } else if (np == 2) {
+          // nearer child on top (popped first); ties keep the left child there
+          const bool near1 = lbs[1] < lbs[0];
+          stack_node[top] = near1 ? rec.ref.x : rec.ref.y;
+          stack_lb[top] = near1 ? lbs[0] : lbs[1];
+          stack_node[top + 1] = near1 ? rec.ref.y : rec.ref.x;
+          stack_lb[top + 1] = near1 ? lbs[1] : lbs[0];
+          top += 2;
+        } else if (np == 1) {
+          stack_node[top] = want0 ? rec.ref.x : rec.ref.y;
+          stack_lb[top] = want0 ? lbs[0] : lbs[1];
+          ++top;
         }
       }
-      const int np = (int)want[0] + (int)want[1];
-      if (top + np > kStackCapacity) {
-        atomicOr(overflow, 1);
-        top = 0;
-      } else if (np == 2) {
-        // nearer child on top (popped first); ties keep the left child there
-        const int near = lbs[1] < lbs[0] ? 1 : 0;
-        stack_node[top] = near ? rec.ref.x : rec.ref.y;
-        stack_lb[top] = lbs[1 - near];
-        stack_node[top + 1] = near ? rec.ref.y : rec.ref.x;
-        stack_lb[top + 1] = lbs[near];
-        top += 2;
-      } else if (np == 1) {
-        stack_node[top] = want[0] ? rec.ref.x : rec.ref.y;
-        stack_lb[top] = want[0] ? lbs[0] : lbs[1];
-        ++top;
+    } else if (climb >= 0) {
+      // ---- one climb step: the sibling of the path under `climb`
+      ++visits;
+      const auto rec = load_node(nodes + climb);
+      const int2 u = __ldg(up + climb);   // (parent link, prefix length of `climb`)
+      float lb;
+      if (visit_child<D, kSkip, kBounds>(rec, 1 - path_side, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
+                                         evals, &lb)) {
+        stack_node[0] = path_side ? rec.ref.x : rec.ref.y;
+        stack_lb[0] = lb;
+        top = 1;
+      }
+      if (radius < prefix_r) {
+        prefix = ball_prefix<D>(q, radius, sc);
+        prefix_r = radius;
+      }
+      if (u.y <= prefix || u.x < 0) {
+        climb = -1;   // every point within the radius lies under this ancestor
+      } else {
+        climb = u.x >> 1;
+        path_side = u.x & 1;
       }
     }
-    if (top == 0) {
-      // the search just proved: no foreign point closer than the final radius
-      if (kBounds && radius >= 0.0) {
+    if (top == 0 && climb < 0) {
+      // the search proved: no foreign point closer than the final radius
+      if (kBounds) {
         const float proven = __double2float_rd(radius);
         const long long slot = q0 + s;
         if (proven > nfn_lb[slot]) nfn_lb[slot] = proven;
@@ -308,7 +344,6 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     if (found) atomicAdd(evals_out + 6, found);     // counters[6]: queries with a candidate
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // Warp-packet variant: the 32 lanes of a warp hold 32 consecutive Morton
