@@ -54,19 +54,52 @@ struct RoundScanStore {
 };
 
 // ------------------------------------------------------------- node labels
+// Also marks the "top pure" nodes: an internal child whose slot range lies in
+// one component while the node itself is mixed.  Every leaf under such a node T
+// has T as its highest single-component ancestor; the marks (T + 1 at the first
+// and the last slot of T's range) are turned into top[s] by k_scan<TopScan*>.
 template <class Node>
 __global__ void k_node_labels(Node* __restrict__ nodes, const int2* __restrict__ range, const int* __restrict__ bprefix,
-                              const int* __restrict__ label, long long m) {
+                              const int* __restrict__ label, long long m, int* __restrict__ mark_lo,
+                              int* __restrict__ mark_hi) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= m) return;
   int2 r = range[i];
-  int lref = nodes[i].ref.x;
-  int gamma = lref >= 0 ? lref : ~lref;
+  const int2 refs = *reinterpret_cast<const int2*>(&nodes[i].ref.x);
+  int gamma = refs.x >= 0 ? refs.x : ~refs.x;
   int bl = bprefix[r.x], bg = bprefix[gamma], bg1 = bprefix[gamma + 1], bh = bprefix[r.y];
   int ll = bg == bl ? label[r.x] : kMixed;
   int rl = bh == bg1 ? label[r.y] : kMixed;
   *reinterpret_cast<int2*>(&nodes[i].ref.z) = make_int2(ll, rl);
+  if (mark_lo && bl != bh) {
+    if (refs.x >= 0 && ll != kMixed) { mark_lo[r.x] = refs.x + 1; mark_hi[gamma] = refs.x + 1; }
+    if (refs.y >= 0 && rl != kMixed) { mark_lo[gamma + 1] = refs.y + 1; mark_hi[r.y] = refs.y + 1; }
+  }
 }
+
+// top[s] = T + 1 for the top pure node T whose range holds slot s, else 0.  The
+// ranges are disjoint, so top[s] = sum_{j <= s} mark_lo[j] - sum_{j < s} mark_hi[j]:
+// an exclusive scan of (mark_lo - mark_hi) plus mark_lo[s], in u64 arithmetic
+// that is exact modulo 2^62 (the scan keeps 62 value bits).  The store clears
+// the marks for the next round (each index is read and cleared by one thread).
+struct TopScanLoad {
+  const int* mark_lo;
+  const int* mark_hi;
+  __device__ unsigned long long operator()(long long i) const {
+    return (unsigned long long)(unsigned)mark_lo[i] - (unsigned long long)(unsigned)mark_hi[i];
+  }
+};
+struct TopScanStore {
+  int* mark_lo;
+  int* mark_hi;
+  int* top;
+  __device__ void operator()(long long i, unsigned long long excl) const {
+    const int lo = mark_lo[i], hi = mark_hi[i];
+    top[i] = (int)((excl + (unsigned long long)(unsigned)lo) & kValueMask);
+    if (lo) mark_lo[i] = 0;
+    if (hi) mark_hi[i] = 0;
+  }
+};
 
 // ------------------------------------------------------------------- merge
 constexpr int kErrNoEdge = 1;     // mst.py:365-376 / 720-721

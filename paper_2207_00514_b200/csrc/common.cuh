@@ -171,16 +171,23 @@ __device__ __forceinline__ unsigned long long morton_of_cells(const unsigned lon
 // point whose distance evaluates to <= r cannot fall outside.
 template <int D>
 __device__ __forceinline__ int ball_prefix(const float* q, double r, const Scene& sc) {
+  // Per axis: the high bits shared by the lattice cells of q - r and q + r.  The
+  // Morton code of axis k's bit j sits at 64-bit position (64 - D*bits) + D*j + k
+  // counted from the top, so the corners' shared code prefix is the minimum of
+  // that position over the axes at their first differing bit (no interleaving).
+  constexpr int bits = D == 3 ? 21 : 31;
   const double scale = D == 3 ? 2097152.0 : 2147483648.0;
   const double rr = __dmul_ru(r, 1.0 + 0x1p-40);
-  unsigned long long clo[3], chi[3];
+  int prefix = 64;
 #pragma unroll
   for (int k = 0; k < D; ++k) {
-    clo[k] = lattice_cell_d(__dsub_rd((double)q[k], rr), sc.lo[k], sc.inv[k], scale);
-    chi[k] = lattice_cell_d(__dadd_ru((double)q[k], rr), sc.lo[k], sc.inv[k], scale);
+    const unsigned long long lo = lattice_cell_d(__dsub_rd((double)q[k], rr), sc.lo[k], sc.inv[k], scale);
+    const unsigned long long hi = lattice_cell_d(__dadd_ru((double)q[k], rr), sc.lo[k], sc.inv[k], scale);
+    const unsigned long long x = lo ^ hi;
+    const int pk = (64 - D * bits) + D * (__clzll((long long)x) - (64 - bits)) + k;
+    prefix = x ? min(prefix, pk) : prefix;
   }
-  const unsigned long long a = morton_of_cells<D>(clo), b = morton_of_cells<D>(chi);
-  return a == b ? 64 : __clzll((long long)(a ^ b));
+  return prefix;
 }
 
 }  // namespace emst

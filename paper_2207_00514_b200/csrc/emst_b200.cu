@@ -115,6 +115,8 @@ struct emst_context {
   // rounds
   DevBuf<int> label, bprefix;
   DevBuf<float> nfn_lb;   // per slot: proven lower bound on the nearest-foreign distance
+  DevBuf<int> mark_lo, mark_hi, top;   // top pure node per slot (T + 1, 0 = none)
+  bool top_valid = false;              // top[] holds this round's values
   DevBuf<unsigned long long> ub;
   DevBuf<EdgeKey> best, shard_keys;
   DevBuf<int> succ, ptr, root, newid, fin;
@@ -353,6 +355,9 @@ void ensure_rounds(emst_context* c, long long n) {
   c->label.ensure(n);
   c->bprefix.ensure(n);
   c->nfn_lb.ensure(n);
+  c->mark_lo.ensure(n);
+  c->mark_hi.ensure(n);
+  c->top.ensure(n);
   c->ub.ensure(n);
   c->best.ensure(n);
   c->succ.ensure(n);
@@ -376,7 +381,10 @@ __global__ void k_iota_int(int* a, long long n) {
 
 // node labels + upper bounds for the current labels (phases 1-2 of a round)
 void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds,
-                   bool binary_labels = false) {
+                   bool binary_labels = false, bool want_top = false) {
+  c->top_valid = false;
+  int* mlo = want_top ? c->mark_lo.p : nullptr;
+  int* mhi = want_top ? c->mark_hi.p : nullptr;
   CK(cudaEventRecord(c->ev_a, c->stream));
   RoundScanLoad load{c->label.p, c->spts.p, c->ub.p, n, c->dim, bounds};
   RoundScanStore store{c->bprefix.p};
@@ -400,10 +408,14 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   if (n > 1 && (!c->wide_w || binary_labels)) {
     if (c->dim == 3)
       launch(c, k_node_labels<Node3>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node3*>(c->nodes.p),
-             (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1);
+             (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1, mlo, mhi);
     else
       launch(c, k_node_labels<Node2>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node2*>(c->nodes.p),
-             (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1);
+             (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1, mlo, mhi);
+    if (want_top) {
+      run_scan(c, n, TopScanLoad{c->mark_lo.p, c->mark_hi.p}, TopScanStore{c->mark_lo.p, c->mark_hi.p, c->top.p}, false);
+      c->top_valid = true;
+    }
   }
   cudaEvent_t ev_c;
   CK(cudaEventCreate(&ev_c));
@@ -459,7 +471,8 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
            (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
            reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1,
-           c->nfn_lb.p, (const int2*)c->up.p, (const int*)c->leaf_parent.p, (const Scene*)c->scene.p);
+           c->nfn_lb.p, (const int2*)c->up.p, (const int*)c->leaf_parent.p, (const Scene*)c->scene.p,
+           c->top_valid ? (const int*)c->top.p : (const int*)nullptr);
   }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
@@ -570,6 +583,8 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   CK(cudaMemsetAsync(c->counters.p, 0, 8 * sizeof(long long), c->stream));
   launch(c, k_iota_int, grid_for(n, 256), 256, 0, c->label.p, n);
   CK(cudaMemsetAsync(c->nfn_lb.p, 0, n * sizeof(float), c->stream));
+  CK(cudaMemsetAsync(c->mark_lo.p, 0, n * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(c->mark_hi.p, 0, n * sizeof(int), c->stream));
   long long comps = n, edges = 0;
   const int max_it = max_iterations(n);
   st->component_counts[0] = n;
@@ -583,7 +598,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     if (st->iterations > max_it) fail(EMST_ERR_ITER, "exceeded the %d-iteration bound for n=%lld", max_it, n);
     CK(cudaMemsetAsync(c->ub.p, 0xff, comps * sizeof(unsigned long long), c->stream));
     CK(cudaMemsetAsync(c->best.p, 0xff, comps * sizeof(EdgeKey), c->stream));
-    round_prepare(c, n, bounds, &ms_labels, &ms_bounds);
+    round_prepare(c, n, bounds, &ms_labels, &ms_bounds, false, (flags & EMST_SUBTREE_SKIP) && comps < n);
     CK(cudaEventRecord(c->ev_a, c->stream));
     c->singleton_round = comps == n;
     c->round = st->iterations;

@@ -75,9 +75,9 @@ k_scan(long long n, unsigned long long* status, unsigned long long* ticket, Load
     unsigned long long agg = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
     // publish, then look back
     if (tile == 0) {
-      if (tid == 0) { st_volatile_u64(&status[0], kFlagPrefix | agg); s_prefix = 0; }
+      if (tid == 0) { st_volatile_u64(&status[0], kFlagPrefix | (agg & kValueMask)); s_prefix = 0; }
     } else {
-      if (tid == 0) st_volatile_u64(&status[tile], kFlagAgg | agg);
+      if (tid == 0) st_volatile_u64(&status[tile], kFlagAgg | (agg & kValueMask));
       unsigned long long excl = 0;
       long long t = tile - 1;
       for (;;) {
@@ -95,7 +95,7 @@ k_scan(long long n, unsigned long long* status, unsigned long long* ticket, Load
         if (pm) break;
         t -= 32;
       }
-      if (tid == 0) { st_volatile_u64(&status[tile], kFlagPrefix | (excl + agg)); s_prefix = excl; }
+      if (tid == 0) { st_volatile_u64(&status[tile], kFlagPrefix | ((excl + agg) & kValueMask)); s_prefix = excl; }
     }
     if (total_out && tid == 0 && base + kScanTile >= n) {
       // the last tile knows the grand total once its prefix is resolved

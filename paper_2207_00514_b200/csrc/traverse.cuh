@@ -20,6 +20,10 @@
 #pragma once
 #include "common.cuh"
 
+// `deep` (the local-memory tail of the traversal stack) is only read below the
+// stack top, i.e. after it was written; nvcc cannot see that.
+#pragma nv_diag_suppress 549
+
 namespace emst {
 
 template <int D>
@@ -74,7 +78,14 @@ constexpr int kTraverseThreads = 256;
 #ifndef EMST_REFILL_IDLE
 #define EMST_REFILL_IDLE 16
 #endif
-constexpr int kTraverseChunk = 128;     // consecutive Morton queries a warp claims at once
+#ifndef EMST_TRAV_CHUNK
+#define EMST_TRAV_CHUNK 64
+#endif
+#ifndef EMST_SMEM_STACK
+#define EMST_SMEM_STACK 12
+#endif
+constexpr int kTraverseChunk = EMST_TRAV_CHUNK;   // consecutive Morton queries a warp claims at once
+constexpr int kSmemStack = EMST_SMEM_STACK;       // stack entries per lane kept in shared memory
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
 constexpr int kRadiusRefresh = 16;      // pops between re-reads of the shared radius
 
@@ -86,7 +97,8 @@ template <int D, bool kSkip, bool kBounds, class Rec>
 __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const float* q, unsigned qp, int comp,
                                             double& radius, float& r2, unsigned long long& best_w,
                                             unsigned long long& best_uv, const unsigned* __restrict__ perm,
-                                            unsigned long long* ub, unsigned long long& evals, float* lb_out) {
+                                            unsigned long long* ub, unsigned& evals, float* lb_out,
+                                            bool enabled = true) {
   const int c = side ? rec.ref.y : rec.ref.x;
   const int cl = side ? rec.ref.w : rec.ref.z;
   float lo[3], hi[3];
@@ -94,7 +106,7 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
   const float lb = box_lb2<D>(q, lo, hi);
   *lb_out = lb;
   const bool same = cl == comp && (c < 0 || kSkip);
-  if (same || lb > r2) return false;
+  if (!enabled || same || lb > r2) return false;
   if (c >= 0) return true;
   ++evals;
   const double w = exact_dist<D>(q, lo);
@@ -125,6 +137,11 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
 // points with its prefix, so nothing outside that ancestor can be within r.
 // In round 1 (radius = distance to a Z-order neighbour) this stops a few levels
 // above the leaf instead of walking ~38 levels down from the root.
+//
+// Stack: the first kSmemStack entries of every lane live in shared memory laid
+// out [depth][thread] (bank = lane for every depth, so lanes at different depths
+// never conflict); deeper entries, rare, spill to a per-thread local array up to
+// the reference's capacity of 64 (bvh.py:36).
 template <int D, bool kSkip, bool kBounds>
 __global__ void __launch_bounds__(kTraverseThreads, EMST_TRAV_MINB)
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
@@ -132,47 +149,57 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
            unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb,
-           const int2* __restrict__ up, const int* __restrict__ leaf_parent, const Scene* __restrict__ scene_ptr) {
+           const int2* __restrict__ up, const int* __restrict__ leaf_parent, const Scene* __restrict__ scene_ptr,
+           const int* __restrict__ top_pure) {
   const unsigned lane = lane_id();
   const unsigned lt = lanemask_lt_u32();
-  const long long total = q1 - q0;
+  const int total = (int)(q1 - q0);
   const Scene sc = *scene_ptr;
 
   // The warp claims kTraverseChunk consecutive Morton slots at a time and stages
-  // their point, label, leaf parent, starting radius and proven nearest-foreign
-  // bound in shared memory with coalesced loads.
-  __shared__ float4 s_pts[kTraverseThreads / 32][kTraverseChunk];
-  __shared__ int s_lab[kTraverseThreads / 32][kTraverseChunk];
-  __shared__ int s_lp[kTraverseThreads / 32][kTraverseChunk];
-  __shared__ unsigned long long s_ub[kTraverseThreads / 32][kTraverseChunk];
-  __shared__ float s_nlb[kTraverseThreads / 32][kTraverseChunk];
+  // their point, label, leaf parent, starting radius, proven nearest-foreign
+  // bound and top pure node in shared memory with coalesced loads.
+  constexpr int W = kTraverseThreads / 32;
+  __shared__ float4 s_pts[W][kTraverseChunk];
+  __shared__ int s_lab[W][kTraverseChunk];
+  __shared__ int s_lp[W][kTraverseChunk];
+  __shared__ unsigned long long s_ub[W][kTraverseChunk];
+  __shared__ float s_nlb[W][kTraverseChunk];
+  __shared__ int s_top[W][kTraverseChunk];
+  __shared__ int2 s_stk[kSmemStack][kTraverseThreads];
+  int2 deep[kStackCapacity - kSmemStack];
   const int wib = threadIdx.x >> 5;
-  long long chunk_base = 0;
-  long long pool_next = 0, pool_end = 0;   // warp-uniform chunk of claimed queries
-  bool exhausted = false;                  // warp-uniform: global work is gone
+  const int tid = threadIdx.x;
+  int chunk_base = 0;
+  int pool_next = 0, pool_end = 0;   // warp-uniform chunk of claimed queries
+  bool exhausted = false;            // warp-uniform: global work is gone
 
-  long long s = -1;
+  int s = -1;
   float q[3] = {0.f, 0.f, 0.f};
   unsigned qp = 0;
   int comp = 0;
   double radius = 0.0;
   float r2 = 0.f;
+  float my_nlb = 0.f;
   unsigned long long best_w = ~0ull, best_uv = ~0ull;
-  int stack_node[kStackCapacity];
-  float stack_lb[kStackCapacity];
   int top = 0;
   int climb = -1;          // ancestor whose sibling subtree is next, -1 = climb over
   int path_side = 0;       // which child of `climb` the query came from
   int prefix = 0;          // Morton prefix shared by the search box
   double prefix_r = 0.0;   // radius `prefix` was computed for
   int since_refresh = 0;
-  unsigned long long evals = 0;
+  unsigned evals = 0, visits = 0, found = 0;
   // a finished query's result waits here until the warp refills, so the
   // L2-latency CAS of many lanes overlaps instead of stalling the warp per lane
   bool pend = false;
   int pcomp = 0;
   unsigned long long pw = 0, puv = 0;
-  unsigned long long visits = 0, found = 0;
+
+  auto stk_get = [&](int i) -> int2 { return i < kSmemStack ? s_stk[i][tid] : deep[i - kSmemStack]; };
+  auto stk_put = [&](int i, int node, float lb) {
+    const int2 e = make_int2(node, __float_as_int(lb));
+    if (i < kSmemStack) s_stk[i][tid] = e; else deep[i - kSmemStack] = e;
+  };
 
   for (;;) {
     // ---- refill idle lanes from the warp's staged chunk of consecutive Morton slots
@@ -194,25 +221,27 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         if ((long long)base >= total) {
           exhausted = true;
         } else {
-          chunk_base = (long long)base;
+          chunk_base = (int)base;
           pool_next = chunk_base;
           pool_end = min(chunk_base + kTraverseChunk, total);
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < kTraverseChunk / 32; ++j) {
-            const long long i = chunk_base + j * 32 + lane;
+            const int i = chunk_base + j * 32 + (int)lane;
             if (i < pool_end) {
-              s_pts[wib][j * 32 + lane] = spts[q0 + i];
-              s_lab[wib][j * 32 + lane] = label[q0 + i];
-              s_lp[wib][j * 32 + lane] = leaf_parent[q0 + i];
-              if (kBounds) s_nlb[wib][j * 32 + lane] = nfn_lb[q0 + i];
+              const long long g = q0 + i;
+              s_pts[wib][j * 32 + lane] = spts[g];
+              s_lab[wib][j * 32 + lane] = label[g];
+              s_lp[wib][j * 32 + lane] = leaf_parent[g];
+              if (kBounds) s_nlb[wib][j * 32 + lane] = nfn_lb[g];
+              if (top_pure) s_top[wib][j * 32 + lane] = top_pure[g];
             }
           }
           if (kBounds) {
             __syncwarp();
 #pragma unroll
             for (int j = 0; j < kTraverseChunk / 32; ++j) {
-              const long long i = chunk_base + j * 32 + lane;
+              const int i = chunk_base + j * 32 + (int)lane;
               if (i < pool_end) s_ub[wib][j * 32 + lane] = __ldcg(&ub[s_lab[wib][j * 32 + lane]]);
             }
           }
@@ -220,13 +249,13 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         }
       }
       if (pool_next < pool_end) {
-        const unsigned rank = __popc(idle & lt);
-        const long long mine = pool_next + (long long)rank;
+        const int rank = __popc(idle & lt);
+        const int mine = pool_next + rank;
         const bool take = s < 0 && mine < pool_end;
-        pool_next = min(pool_end, pool_next + (long long)n_idle);
+        pool_next = min(pool_end, pool_next + n_idle);
         if (take) {
           s = mine;
-          const int k = (int)(mine - chunk_base);
+          const int k = mine - chunk_base;
           const float4 qv = s_pts[wib][k];
           q[0] = qv.x; q[1] = qv.y; q[2] = qv.z;
           qp = __float_as_uint(qv.w);
@@ -242,10 +271,26 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           prefix = radius < 1e300 ? ball_prefix<D>(q, radius, sc) : -1;
           prefix_r = radius;
           since_refresh = kRadiusRefresh / 2;   // staged radius may be stale: refresh early
+          my_nlb = kBounds ? s_nlb[wib][k] : 0.f;
           // A previous round proved every foreign point is farther than nfn_lb[s]
           // (foreign sets only shrink, so that stays true).  If that already
           // exceeds the radius, this query cannot find an edge: done.
-          if (kBounds && (double)s_nlb[wib][k] > radius) climb = -1;
+          if (kBounds && (double)my_nlb > radius) climb = -1;
+          // Every leaf under the query's top pure node T is in its own component:
+          // the climb starts above T, and if the search box's prefix already lies
+          // inside T there is nothing foreign within the radius at all.
+          if (top_pure && climb >= 0) {
+            const int t = s_top[wib][k];
+            if (t > 0) {
+              const int2 ut = __ldg(up + (t - 1));
+              if (ut.y <= prefix || ut.x < 0) {
+                climb = -1;
+              } else {
+                climb = ut.x >> 1;
+                path_side = ut.x & 1;
+              }
+            }
+          }
         }
       }
     }
@@ -256,66 +301,76 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       const double shared = bits_to_radius(__ldcg(&ub[comp]));
       if (shared < radius) { radius = shared; r2 = prune_r2(shared); }
     }
-    if (top > 0) {
-      // ---- explore a parked sibling subtree top-down
+    // ---- one node visit per iteration, the same code for both kinds of step so
+    // that lanes popping a parked subtree and lanes climbing do not diverge:
+    //   pop:   both children of a parked node (top-down, nearest first)
+    //   climb: only the sibling of the path under ancestor `climb`
+    // Parked entries the radius has since pruned are dropped first.
+    int2 e = make_int2(-1, 0);
+    while (top > 0) {
+      e = stk_get(top - 1);
+      if (__int_as_float(e.y) <= r2) break;
       --top;
-      if (stack_lb[top] <= r2) {
-        ++visits;
-        const auto rec = load_node(nodes + stack_node[top]);
-        float lbs[2];
-        const bool w0 = visit_child<D, kSkip, kBounds>(rec, 0, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
-                                                       evals, &lbs[0]);
-        const bool w1 = visit_child<D, kSkip, kBounds>(rec, 1, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
-                                                       evals, &lbs[1]);
-        const bool want0 = w0 && lbs[0] <= r2, want1 = w1 && lbs[1] <= r2;
-        const int np = (int)want0 + (int)want1;
-        if (top + np > kStackCapacity) {
-          atomicOr(overflow, 1);
-          top = 0;
-          climb = -1;
-        } else if (np == 2) {
-          // nearer child on top (popped first); ties keep the left child there
-          const bool near1 = lbs[1] < lbs[0];
-          stack_node[top] = near1 ? rec.ref.x : rec.ref.y;
-          stack_lb[top] = near1 ? lbs[0] : lbs[1];
-          stack_node[top + 1] = near1 ? rec.ref.y : rec.ref.x;
-          stack_lb[top + 1] = near1 ? lbs[1] : lbs[0];
-          top += 2;
-        } else if (np == 1) {
-          stack_node[top] = want0 ? rec.ref.x : rec.ref.y;
-          stack_lb[top] = want0 ? lbs[0] : lbs[1];
-          ++top;
-        }
-      }
-    } else if (climb >= 0) {
-      // ---- one climb step: the sibling of the path under `climb`
+      e.x = -1;
+    }
+    int node;
+    unsigned sides;
+    const bool climbing = top == 0;
+    if (!climbing) {
+      --top;
+      node = e.x;
+      sides = 3u;
+    } else {
+      node = climb;              // -1 when the climb is over: nothing to visit
+      sides = 2u >> path_side;   // the side that is not on the path
+    }
+    if (node >= 0) {
       ++visits;
-      const auto rec = load_node(nodes + climb);
-      const int2 u = __ldg(up + climb);   // (parent link, prefix length of `climb`)
-      float lb;
-      if (visit_child<D, kSkip, kBounds>(rec, 1 - path_side, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
-                                         evals, &lb)) {
-        stack_node[0] = path_side ? rec.ref.x : rec.ref.y;
-        stack_lb[0] = lb;
-        top = 1;
+      const auto rec = load_node(nodes + node);
+      int2 u = make_int2(-1, 0);
+      if (climbing) u = __ldg(up + node);   // (parent link, prefix length of `climb`)
+      float lb0, lb1;
+      const bool w0 = visit_child<D, kSkip, kBounds>(rec, 0, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
+                                                     evals, &lb0, sides & 1u);
+      const bool w1 = visit_child<D, kSkip, kBounds>(rec, 1, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
+                                                     evals, &lb1, sides & 2u);
+      const bool want0 = w0 && lb0 <= r2, want1 = w1 && lb1 <= r2;
+      const int np = (int)want0 + (int)want1;
+      if (top + np > kStackCapacity) {
+        atomicOr(overflow, 1);
+        top = 0;
+        climb = -1;
+      } else if (np == 2) {
+        // nearer child on top (popped first); ties keep the left child there
+        const bool near1 = lb1 < lb0;
+        stk_put(top, near1 ? rec.ref.x : rec.ref.y, near1 ? lb0 : lb1);
+        stk_put(top + 1, near1 ? rec.ref.y : rec.ref.x, near1 ? lb1 : lb0);
+        top += 2;
+      } else if (np == 1) {
+        stk_put(top, want0 ? rec.ref.x : rec.ref.y, want0 ? lb0 : lb1);
+        ++top;
       }
-      if (radius < prefix_r) {
-        prefix = ball_prefix<D>(q, radius, sc);
-        prefix_r = radius;
-      }
-      if (u.y <= prefix || u.x < 0) {
-        climb = -1;   // every point within the radius lies under this ancestor
-      } else {
-        climb = u.x >> 1;
-        path_side = u.x & 1;
+      if (climbing && climb >= 0) {
+        // A prefix computed for a larger radius is still a valid (earlier-stopping
+        // is never required) bound; refresh it only when the climb would go on
+        // and the radius has at least halved since.
+        if (u.y > prefix && radius <= 0.5 * prefix_r) {
+          prefix = ball_prefix<D>(q, radius, sc);
+          prefix_r = radius;
+        }
+        if (u.y <= prefix || u.x < 0) {
+          climb = -1;   // every point within the radius lies under this ancestor
+        } else {
+          climb = u.x >> 1;
+          path_side = u.x & 1;
+        }
       }
     }
     if (top == 0 && climb < 0) {
       // the search proved: no foreign point closer than the final radius
       if (kBounds) {
         const float proven = __double2float_rd(radius);
-        const long long slot = q0 + s;
-        if (proven > nfn_lb[slot]) nfn_lb[slot] = proven;
+        if (proven > my_nlb) nfn_lb[q0 + s] = proven;
       }
       if (best_uv != ~0ull) {
         ++found;
@@ -332,16 +387,17 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       s = -1;
     }
   }
+  unsigned long long ev64 = evals, vi64 = visits, fo64 = found;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    evals += __shfl_xor_sync(0xffffffffu, evals, o);
-    visits += __shfl_xor_sync(0xffffffffu, visits, o);
-    found += __shfl_xor_sync(0xffffffffu, found, o);
+    ev64 += __shfl_xor_sync(0xffffffffu, ev64, o);
+    vi64 += __shfl_xor_sync(0xffffffffu, vi64, o);
+    fo64 += __shfl_xor_sync(0xffffffffu, fo64, o);
   }
   if (lane == 0) {
-    if (evals) atomicAdd(evals_out, evals);
-    if (visits) atomicAdd(evals_out + 5, visits);   // counters[5]: node visits
-    if (found) atomicAdd(evals_out + 6, found);     // counters[6]: queries with a candidate
+    if (ev64) atomicAdd(evals_out, ev64);
+    if (vi64) atomicAdd(evals_out + 5, vi64);   // counters[5]: node visits
+    if (fo64) atomicAdd(evals_out + 6, fo64);   // counters[6]: queries with a candidate
   }
 }
 
