@@ -24,33 +24,113 @@
 namespace emst {
 
 // ---------------------------------------------------------------- bounds + B
-struct RoundScanLoad {
+// One scan over the labels: the boundary flags label[i] != label[i+1] are
+// prefix-summed into B[i] (exclusive), and with bounds on, each boundary pair
+// seeds both components' upper bounds with its exact f64 weight (u64 min of
+// the bit pattern; order-independent, so equal to the serial fold of
+// mst.py:198-224).  The 8 items of a thread issue their point loads together,
+// then their bound reads, and only the pairs that can still lower a bound
+// send an atomic (late rounds funnel many boundaries into few components).
+// Lower ub[l] to w for the (l, w) pairs of every lane (l < 0: none).  Dense
+// warps (early rounds: distinct labels) read each bound and send an atomic
+// only where it can still lower it.  Sparse warps (late rounds: few
+// components, many boundaries per component) first reduce per label across
+// the warp, so a component receives one atomic per warp instead of one per
+// boundary.
+template <int K>
+__device__ __forceinline__ void apply_bound_updates(int* ul, unsigned long long* uw, unsigned long long* ub) {
+  unsigned pending = 0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) pending |= ul[j] >= 0 ? 1u << j : 0u;
+  const unsigned busy = __ballot_sync(0xffffffffu, pending != 0);
+  if (__popc(busy) > 8) {
+    unsigned long long cur[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) cur[j] = ul[j] >= 0 ? __ldcg(&ub[ul[j]]) : 0ull;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (uw[j] < cur[j]) atomicMin(&ub[ul[j]], uw[j]);
+    return;
+  }
+  const unsigned lane = lane_id();
+  for (;;) {
+    const unsigned has = __ballot_sync(0xffffffffu, pending != 0);
+    if (!has) break;
+    const int leader = __ffs(has) - 1;
+    const int first = pending ? __ffs(pending) - 1 : 0;
+    int mine_l = -1;
+#pragma unroll
+    for (int j = 0; j < K; ++j) if (j == first) mine_l = ul[j];
+    const int L = __shfl_sync(0xffffffffu, mine_l, leader);
+    unsigned long long w = ~0ull;
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if ((pending >> j & 1u) && ul[j] == L) { w = min(w, uw[j]); pending &= ~(1u << j); }
+    const unsigned hi = __reduce_min_sync(0xffffffffu, (unsigned)(w >> 32));
+    const unsigned lo = __reduce_min_sync(0xffffffffu, (unsigned)(w >> 32) == hi ? (unsigned)w : 0xffffffffu);
+    if ((int)lane == leader) {
+      const unsigned long long m = ((unsigned long long)hi << 32) | lo;
+      if (m < __ldcg(&ub[L])) atomicMin(&ub[L], m);
+    }
+  }
+}
+
+struct RoundScanOp {
+  using T = unsigned;
   const int* label;
   const float4* spts;
   unsigned long long* ub;
+  int* bprefix;
   long long n;
   int dim;
   bool bounds;
-  __device__ unsigned long long operator()(long long i) const {
-    if (i + 1 >= n) return 0ull;
-    int la = label[i], lb = label[i + 1];
-    if (la == lb) return 0ull;
-    if (bounds) {
-      float4 a = spts[i], b = spts[i + 1];
-      float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
-      double w = dim == 3 ? exact_dist<3>(pa, pb) : exact_dist<2>(pa, pb);
-      unsigned long long bits = (unsigned long long)__double_as_longlong(w);
-      // late rounds funnel many boundary pairs into few components: read first,
-      // and only issue the atomic when it can still lower the bound
-      if (bits < __ldcg(&ub[la])) atomicMin(&ub[la], bits);
-      if (bits < __ldcg(&ub[lb])) atomicMin(&ub[lb], bits);
+  __device__ void load(long long i0, int cnt, unsigned* v) const {
+    int lab[kScanItems + 1];
+#pragma unroll
+    for (int j = 0; j <= kScanItems; ++j) lab[j] = 0;
+    load8(label, i0, cnt, lab);
+    if (i0 + kScanItems < n) lab[kScanItems] = __ldg(label + i0 + kScanItems);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) v[j] = (i0 + j + 1 < n && lab[j] != lab[j + 1]) ? 1u : 0u;
+    if (!bounds) return;   // (warp-uniform)
+    unsigned long long wb[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      wb[j] = ~0ull;
+      if (v[j]) {
+        const float4 a = __ldg(spts + i0 + j), b = __ldg(spts + i0 + j + 1);
+        const float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
+        const double w = dim == 3 ? exact_dist<3>(pa, pb) : exact_dist<2>(pa, pb);
+        wb[j] = (unsigned long long)__double_as_longlong(w);
+      }
     }
-    return 1ull;
+    // One update per run of equal labels among the thread's 9 slots: the min of
+    // the (at most two) boundary weights around the run.
+    int ul[kScanItems + 1];
+    unsigned long long uw[kScanItems + 1];
+    // (slot kScanItems is the next thread's first; it exists iff i0 + 8 < n)
+    const int last = i0 + kScanItems < n ? kScanItems : cnt - 1;
+    unsigned long long run = ~0ull;
+#pragma unroll
+    for (int j = 0; j <= kScanItems; ++j) {
+      if (j > 0 && v[j - 1]) run = min(run, wb[j - 1]);          // boundary left of slot j
+      if (j < kScanItems && v[j]) run = min(run, wb[j]);         // boundary right of slot j
+      const bool run_ends = j == last || (j < kScanItems && v[j]);
+      ul[j] = j <= last && run_ends && run != ~0ull ? lab[j] : -1;
+      uw[j] = run;
+      if (run_ends) run = ~0ull;
+    }
+    apply_bound_updates<kScanItems + 1>(ul, uw, ub);   // every lane of the warp takes part
   }
-};
-struct RoundScanStore {
-  int* bprefix;
-  __device__ void operator()(long long i, unsigned long long excl) const { bprefix[i] = (int)excl; }
+  __device__ void store(long long i0, int cnt, const unsigned* v, unsigned ex) const {
+    int out[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      out[j] = (int)ex;
+      ex += v[j];
+    }
+    store8(bprefix, i0, cnt, out);
+  }
 };
 
 // ------------------------------------------------------------- node labels
@@ -79,25 +159,39 @@ __global__ void k_node_labels(Node* __restrict__ nodes, const int2* __restrict__
 
 // top[s] = T + 1 for the top pure node T whose range holds slot s, else 0.  The
 // ranges are disjoint, so top[s] = sum_{j <= s} mark_lo[j] - sum_{j < s} mark_hi[j]:
-// an exclusive scan of (mark_lo - mark_hi) plus mark_lo[s], in u64 arithmetic
-// that is exact modulo 2^62 (the scan keeps 62 value bits).  The store clears
-// the marks for the next round (each index is read and cleared by one thread).
-struct TopScanLoad {
-  const int* mark_lo;
-  const int* mark_hi;
-  __device__ unsigned long long operator()(long long i) const {
-    return (unsigned long long)(unsigned)mark_lo[i] - (unsigned long long)(unsigned)mark_hi[i];
-  }
-};
-struct TopScanStore {
+// an exclusive scan of (mark_lo - mark_hi) plus mark_lo[s], in wrapping u32
+// arithmetic (exact, every true prefix is in [0, 2^30)).  The store clears the
+// marks for the next round (each index is read and cleared by one thread).
+struct TopScanOp {
+  using T = unsigned;
   int* mark_lo;
   int* mark_hi;
   int* top;
-  __device__ void operator()(long long i, unsigned long long excl) const {
-    const int lo = mark_lo[i], hi = mark_hi[i];
-    top[i] = (int)((excl + (unsigned long long)(unsigned)lo) & kValueMask);
-    if (lo) mark_lo[i] = 0;
-    if (hi) mark_hi[i] = 0;
+  __device__ void load(long long i0, int cnt, unsigned* v) const {
+    int lo[kScanItems], hi[kScanItems];
+    load8(mark_lo, i0, cnt, lo);
+    load8(mark_hi, i0, cnt, hi);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) v[j] = j < cnt ? (unsigned)lo[j] - (unsigned)hi[j] : 0u;
+  }
+  __device__ void store(long long i0, int cnt, const unsigned* v, unsigned ex) const {
+    int out[kScanItems];
+    unsigned nz = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      // v[j] = lo - hi; the start mark lo is 0 unless a range opens here, and a
+      // range of >= 2 slots never opens and closes on the same slot
+      const int lo = j < cnt ? __ldg(mark_lo + i0 + j) : 0;
+      out[j] = (int)(ex + (unsigned)lo);
+      ex += v[j];
+      nz |= v[j];
+    }
+    store8(top, i0, cnt, out);
+    if (nz) {
+#pragma unroll
+      for (int j = 0; j < kScanItems; ++j)
+        if (j < cnt && v[j]) { mark_lo[i0 + j] = 0; mark_hi[i0 + j] = 0; }
+    }
   }
 };
 
@@ -148,19 +242,11 @@ __global__ void k_merge_jump(int* ptr, long long c, int* __restrict__ root, int*
   root[k] = x;
 }
 
-// flags packed for one scan: bit 0..30 "emits its edge", bit 31.. "is a root"
-struct MergeScanLoad {
-  const int* succ;
-  const int* root;
-  __device__ unsigned long long operator()(long long k) const {
-    int y = succ[k];
-    bool mutual = succ[y] == (int)k;
-    unsigned long long edge = (mutual && y < (int)k) ? 0ull : 1ull;   // mst.py:416-423
-    unsigned long long is_root = root[k] == (int)k ? 1ull : 0ull;
-    return edge | (is_root << 31);
-  }
-};
-struct MergeScanStore {
+// flags packed for one scan: bits 0..30 "emits its edge" (mst.py:416-423),
+// bits 31..61 "is a cluster root"; the store appends the emitted edges and
+// gives every root its new dense id.
+struct MergeScanOp {
+  using T = unsigned long long;
   const int* succ;
   const int* root;
   const EdgeKey* best;
@@ -169,17 +255,37 @@ struct MergeScanStore {
   unsigned long long* ew;
   long long edge_base;
   int* newid;
-  __device__ void operator()(long long k, unsigned long long excl) const {
-    int y = succ[k];
-    bool mutual = succ[y] == (int)k;
-    if (!(mutual && y < (int)k)) {
-      long long at = edge_base + (long long)(excl & 0x7fffffffull);
-      EdgeKey e = best[k];
-      eu[at] = (unsigned)(e.uv >> 32);
-      ev[at] = (unsigned)(e.uv & 0xffffffffu);
-      ew[at] = e.w;
+  __device__ void load(long long i0, int cnt, unsigned long long* v) const {
+    int y[kScanItems], r[kScanItems], yy[kScanItems];
+    load8(succ, i0, cnt, y);
+    load8(root, i0, cnt, r);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) yy[j] = j < cnt ? __ldg(succ + y[j]) : -1;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      if (j >= cnt) continue;
+      const int k = (int)(i0 + j);
+      const bool mutual = yy[j] == k;
+      const unsigned long long edge = (mutual && y[j] < k) ? 0ull : 1ull;
+      const unsigned long long is_root = r[j] == k ? 1ull : 0ull;
+      v[j] = edge | (is_root << 31);
     }
-    if (root[k] == (int)k) newid[k] = (int)(excl >> 31);
+  }
+  __device__ void store(long long i0, int cnt, const unsigned long long* v, unsigned long long ex) const {
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      if (j >= cnt) continue;
+      const long long k = i0 + j;
+      if (v[j] & 1ull) {
+        const long long at = edge_base + (long long)(ex & 0x7fffffffull);
+        const EdgeKey e = best[k];
+        eu[at] = (unsigned)(e.uv >> 32);
+        ev[at] = (unsigned)(e.uv & 0xffffffffu);
+        ew[at] = e.w;
+      }
+      if (v[j] >> 31) newid[k] = (int)(ex >> 31);
+      ex += v[j];
+    }
   }
 };
 

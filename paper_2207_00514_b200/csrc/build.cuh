@@ -217,9 +217,11 @@ __global__ void k_refit(const float4* __restrict__ spts, long long n, Node* node
   for (;;) {
     int node = link >> 1, side = link & 1;
     put_child_box(nodes, node, side, lo, hi);
-    __threadfence();
-    if (atomicAdd(&arrivals[node], 1u) == 0) return;   // first arrival: sibling not done yet
-    __threadfence();
+    // acq_rel: the first arrival's box is released by its increment and the
+    // second arrival acquires it with its own (no full fences needed)
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&arrivals[node]) : "memory");
+    if (prev == 0) return;   // first arrival: sibling not done yet
     get_union_box(nodes, node, lo, hi);
     if (node == 0) {
       for (int k = 0; k < 3; ++k) { root_box->lo[k] = lo[k]; root_box->hi[k] = hi[k]; }

@@ -49,16 +49,18 @@ __device__ __forceinline__ bool key_less(unsigned long long w, unsigned long lon
   return w < bw || (w == bw && uv < buv);
 }
 
-// Lexicographic 128-bit atomic min via the sm_90+ 16-byte CAS.  Reads first and
-// only CASes while strictly smaller, so contended components rarely loop.
+// Lexicographic 128-bit atomic min via the sm_90+ 16-byte CAS.  The first CAS
+// expects the empty key (the common case for the first candidate of a
+// component); a failed CAS returns the current key, and the loop only retries
+// while ours is strictly smaller, so contended components rarely loop.
 __device__ __forceinline__ void atomic_min_key(EdgeKey* addr, unsigned long long w, unsigned long long uv) {
   EdgeKey cur;
-  // one 16-byte L2 read; a torn pair only costs one failed CAS
-  asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(cur.uv), "=l"(cur.w) : "l"(addr));
+  cur.uv = ~0ull;
+  cur.w = ~0ull;
+  EdgeKey mine;
+  mine.w = w;
+  mine.uv = uv;
   while (key_less(w, uv, cur.w, cur.uv)) {
-    EdgeKey mine;
-    mine.w = w;
-    mine.uv = uv;
     EdgeKey old = atomicCAS(addr, cur, mine);
     if (old.w == cur.w && old.uv == cur.uv) return;
     cur = old;

@@ -19,7 +19,6 @@
 #include "build.cuh"
 #include "radix_sort.cuh"
 #include "scan.cuh"
-#include "wide.cuh"
 
 using namespace emst;
 
@@ -80,8 +79,6 @@ struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
   bool singleton_round = false;   // every component is one point (round 1 of a solve)
   int round = 0;                  // 1-based Boruvka round of the running solve (0 outside)
-  int packet_from = 1 << 30;      // rounds >= this use the warp-packet traversal (EMST_PACKET_FROM)
-  int traversal = 0;   // EMST_TRAVERSAL: 0 lane (binary), 1 packet (binary), 2 wide4, 3 wide8
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
@@ -107,11 +104,6 @@ struct emst_context {
   DevBuf<int2> up;   // (parent link, prefix length) per internal node
   DevBuf<unsigned> arrivals;
   DevBuf<Box3> root_box;
-  DevBuf<unsigned char> wnodes;   // wide traversal tree (WideNode<D, W>)
-  DevBuf<int2> wrange;
-  DevBuf<int> wtmp;               // depth / ancestor ping-pong, kept-node index
-  long long mw = 0;               // wide node count
-  int wide_w = 0;                 // children per wide node (0: no wide tree)
   // rounds
   DevBuf<int> label, bprefix;
   DevBuf<float> nfn_lb;   // per slot: proven lower bound on the nearest-foreign distance
@@ -153,15 +145,14 @@ void read_counters(emst_context* c) {
 }
 
 // ------------------------------------------------------------------- scan
-template <class L, class S>
-unsigned long long run_scan(emst_context* c, long long n, L load, S store, bool want_total) {
+template <class Op>
+void run_scan(emst_context* c, long long n, Op op, bool want_total) {
   long long tiles = scan_tiles(n);
   c->scan_scratch.ensure(tiles + 1);
   CK(cudaMemsetAsync(c->scan_scratch.p, 0, (tiles + 1) * sizeof(unsigned long long), c->stream));
   unsigned long long* total = reinterpret_cast<unsigned long long*>(dev_counter(c, 1));
-  launch(c, k_scan<L, S>, (unsigned)tiles, kScanThreads, 0, n, c->scan_scratch.p + 1, c->scan_scratch.p, load, store,
+  launch(c, k_scan<Op>, (unsigned)tiles, kScanThreads, 0, n, c->scan_scratch.p + 1, c->scan_scratch.p, op,
          want_total ? total : (unsigned long long*)nullptr);
-  return 0;
 }
 
 // ------------------------------------------------------------------- sort
@@ -248,37 +239,6 @@ void ensure_build(emst_context* c, long long n, int d) {
   c->nodes_stride = node_bytes;
 }
 
-template <int D, int L>
-void build_wide_t(emst_context* c, long long n) {
-  constexpr int W = 1 << L;
-  using Node = typename NodeOf<D>::type;
-  const long long m = n - 1;
-  c->wtmp.ensure((size_t)5 * m);
-  int *anc0 = c->wtmp.p, *dep0 = anc0 + m, *anc1 = dep0 + m, *dep1 = anc1 + m, *widx = dep1 + m;
-  launch(c, k_depth_init, grid_for(m, 256), 256, 0, (const int*)c->node_parent.p, m, anc0, dep0);
-  for (int it = 0; it < 8; ++it) {   // 2^8 > any tree height
-    launch(c, k_depth_jump, grid_for(m, 256), 256, 0, (const int*)anc0, (const int*)dep0, m, anc1, dep1);
-    std::swap(anc0, anc1);
-    std::swap(dep0, dep1);
-  }
-  KeptLoad<L> load{dep0};
-  KeptStore<L> store{dep0, widx};
-  run_scan(c, m, load, store, true);
-  read_counters(c);
-  const long long mw = c->host_counters[1];
-  c->wnodes.ensure((size_t)mw * sizeof(WideNode<D, W>));
-  c->wrange.ensure((size_t)mw * W);
-  launch(c, k_collapse<D, L>, grid_for(m, 128), 128, 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p),
-         (const int2*)c->range.p, (const int*)widx, m, reinterpret_cast<WideNode<D, W>*>(c->wnodes.p), c->wrange.p);
-  c->mw = mw;
-  c->wide_w = W;
-}
-
-void build_wide(emst_context* c, long long n, int d, int L) {
-  if (d == 3) { if (L == 3) build_wide_t<3, 3>(c, n); else build_wide_t<3, 2>(c, n); }
-  else { if (L == 3) build_wide_t<2, 3>(c, n); else build_wide_t<2, 2>(c, n); }
-}
-
 // Validates and builds the hierarchy; the points must already be in c->pts
 // (or at `dev_pts`).  Returns after a sync with the scene checked.
 void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
@@ -332,8 +292,6 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
     launch(c, k_pack_up, grid_for(n - 1, 256), 256, 0, (const int*)c->node_parent.p, (const int*)c->node_delta.p, n - 1,
            c->up.p);
   c->tree_valid = true;
-  c->wide_w = 0;
-  if (n > 1 && c->traversal >= 2) build_wide(c, n, d, c->traversal == 3 ? 3 : 2);
 }
 
 const float* stage_points(emst_context* c, const float* pts, long long n, int d, int flags, emst_stats* st) {
@@ -381,31 +339,14 @@ __global__ void k_iota_int(int* a, long long n) {
 
 // node labels + upper bounds for the current labels (phases 1-2 of a round)
 void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds,
-                   bool binary_labels = false, bool want_top = false) {
+                   bool want_top = false) {
   c->top_valid = false;
   int* mlo = want_top ? c->mark_lo.p : nullptr;
   int* mhi = want_top ? c->mark_hi.p : nullptr;
   CK(cudaEventRecord(c->ev_a, c->stream));
-  RoundScanLoad load{c->label.p, c->spts.p, c->ub.p, n, c->dim, bounds};
-  RoundScanStore store{c->bprefix.p};
-  run_scan(c, n, load, store, false);
+  run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds}, false);
   CK(cudaEventRecord(c->ev_b, c->stream));
-  if (n > 1 && c->wide_w) {
-    const long long t = c->mw * c->wide_w;
-    if (c->dim == 3 && c->wide_w == 4)
-      launch(c, k_wide_labels<3, 4>, grid_for(t, 256), 256, 0, reinterpret_cast<WideNode<3, 4>*>(c->wnodes.p),
-             (const int2*)c->wrange.p, (const int*)c->bprefix.p, (const int*)c->label.p, c->mw);
-    else if (c->dim == 3)
-      launch(c, k_wide_labels<3, 8>, grid_for(t, 256), 256, 0, reinterpret_cast<WideNode<3, 8>*>(c->wnodes.p),
-             (const int2*)c->wrange.p, (const int*)c->bprefix.p, (const int*)c->label.p, c->mw);
-    else if (c->wide_w == 4)
-      launch(c, k_wide_labels<2, 4>, grid_for(t, 256), 256, 0, reinterpret_cast<WideNode<2, 4>*>(c->wnodes.p),
-             (const int2*)c->wrange.p, (const int*)c->bprefix.p, (const int*)c->label.p, c->mw);
-    else
-      launch(c, k_wide_labels<2, 8>, grid_for(t, 256), 256, 0, reinterpret_cast<WideNode<2, 8>*>(c->wnodes.p),
-             (const int2*)c->wrange.p, (const int*)c->bprefix.p, (const int*)c->label.p, c->mw);
-  }
-  if (n > 1 && (!c->wide_w || binary_labels)) {
+  if (n > 1) {
     if (c->dim == 3)
       launch(c, k_node_labels<Node3>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node3*>(c->nodes.p),
              (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1, mlo, mhi);
@@ -413,7 +354,7 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
       launch(c, k_node_labels<Node2>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node2*>(c->nodes.p),
              (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1, mlo, mhi);
     if (want_top) {
-      run_scan(c, n, TopScanLoad{c->mark_lo.p, c->mark_hi.p}, TopScanStore{c->mark_lo.p, c->mark_hi.p, c->top.p}, false);
+      run_scan(c, n, TopScanOp{c->mark_lo.p, c->mark_hi.p, c->top.p}, false);
       c->top_valid = true;
     }
   }
@@ -443,30 +384,7 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
   unsigned long long* work = reinterpret_cast<unsigned long long*>(dev_counter(c, 4));
   CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
   CK(cudaEventRecord(c->tv_a, c->stream));
-  if (c->wide_w) {
-    if (c->wide_w == 4) {
-      auto kw = k_traverse_wide<D, 4, S, B>;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kw, kTraverseThreads, 0));
-      const unsigned g = (unsigned)std::max<long long>(1, std::min<long long>((long long)c->num_sms * std::max(per_sm, 1), blocks_needed));
-      launch(c, kw, g, kTraverseThreads, 0, (const WideNode<D, 4>*)reinterpret_cast<WideNode<D, 4>*>(c->wnodes.p),
-             (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
-             (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
-             reinterpret_cast<int*>(dev_counter(c, 3)), work);
-    } else {
-      auto kw = k_traverse_wide<D, 8, S, B>;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kw, kTraverseThreads, 0));
-      const unsigned g = (unsigned)std::max<long long>(1, std::min<long long>((long long)c->num_sms * std::max(per_sm, 1), blocks_needed));
-      launch(c, kw, g, kTraverseThreads, 0, (const WideNode<D, 8>*)reinterpret_cast<WideNode<D, 8>*>(c->wnodes.p),
-             (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
-             (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
-             reinterpret_cast<int*>(dev_counter(c, 3)), work);
-    }
-  } else if (c->traversal == 1 || c->round >= c->packet_from) {
-    launch(c, k_traverse_packet<D, S, B>, grid_for(q1 - q0, kTraverseThreads), kTraverseThreads, 0,
-           (const Node*)reinterpret_cast<Node*>(c->nodes.p), (const float4*)c->spts.p, (const unsigned*)c->perm.p,
-           (const int*)c->label.p, c->ub.p, out, q0, q1, (const Box3*)c->root_box.p,
-           reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), reinterpret_cast<int*>(dev_counter(c, 3)));
-  } else {
+  {
     launch(c, kernel, grid, kTraverseThreads, 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p),
            (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
@@ -529,9 +447,8 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
          (const unsigned*)c->iperm.p, c->succ.p, err);
   launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
   launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, c->root.p, err);
-  MergeScanLoad load{c->succ.p, c->root.p};
-  MergeScanStore store{c->succ.p, c->root.p, c->best.p, c->eu.p, c->ev.p, c->ew.p, edge_base, c->newid.p};
-  run_scan(c, comps, load, store, true);
+  run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->eu.p, c->ev.p, c->ew.p, edge_base, c->newid.p},
+           true);
   launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->root.p, (const int*)c->newid.p, comps, c->fin.p);
   launch(c, k_relabel, grid_for(n, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
   read_counters(c);
@@ -598,7 +515,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     if (st->iterations > max_it) fail(EMST_ERR_ITER, "exceeded the %d-iteration bound for n=%lld", max_it, n);
     CK(cudaMemsetAsync(c->ub.p, 0xff, comps * sizeof(unsigned long long), c->stream));
     CK(cudaMemsetAsync(c->best.p, 0xff, comps * sizeof(EdgeKey), c->stream));
-    round_prepare(c, n, bounds, &ms_labels, &ms_bounds, false, (flags & EMST_SUBTREE_SKIP) && comps < n);
+    round_prepare(c, n, bounds, &ms_labels, &ms_bounds, (flags & EMST_SUBTREE_SKIP) && comps < n);
     CK(cudaEventRecord(c->ev_a, c->stream));
     c->singleton_round = comps == n;
     c->round = st->iterations;
@@ -693,9 +610,6 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (world < 1 || rank < 0 || rank >= world) fail(EMST_ERR_PARAM, "bad rank %d / world %d", rank, world);
     c = new emst_context();
     c->device = device;
-    if (const char* t = getenv("EMST_PACKET_FROM")) c->packet_from = atoi(t);
-    if (const char* t = getenv("EMST_TRAVERSAL"))
-      c->traversal = !strcmp(t, "wide4") ? 2 : !strcmp(t, "packet") ? 1 : !strcmp(t, "wide8") ? 3 : 0;
     c->rank = rank;
     c->world = world;
     set_device(c);
@@ -732,7 +646,6 @@ int emst_context_destroy(emst_context* c) {
   c->sort_hist.release(); c->sort_off.release(); c->sort_status.release(); c->sort_misc.release();
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
   c->node_parent.release(); c->leaf_parent.release(); c->node_delta.release(); c->up.release(); c->arrivals.release(); c->root_box.release();
-  c->wnodes.release(); c->wrange.release(); c->wtmp.release();
   c->label.release(); c->bprefix.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->eu.release(); c->ev.release(); c->ew.release(); c->xw.release(); c->xuv.release();
@@ -963,7 +876,7 @@ int emst_reduce_labels(emst_context* c, const float* pts, int64_t n, int32_t d, 
     build_tree(c, dp, n, d);
     if (n == 1) return EMST_OK;
     prepare_labels_from_host(c, labels, n);
-    round_prepare(c, n, false, nullptr, nullptr, true);
+    round_prepare(c, n, false, nullptr, nullptr);
     DevBuf<long long> il;
     il.ensure(n - 1);
     if (d == 3)

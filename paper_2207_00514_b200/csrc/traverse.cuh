@@ -89,16 +89,56 @@ constexpr int kSmemStack = EMST_SMEM_STACK;       // stack entries per lane kept
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
 constexpr int kRadiusRefresh = 16;      // pops between re-reads of the shared radius
 
+// f32 upper bound of |q - p|^2 (every operation rounded toward +inf).
+template <int D>
+__device__ __forceinline__ float point_ub2(const float* q, const float* p) {
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float g = fmaxf(__fsub_ru(q[k], p[k]), __fsub_ru(p[k], q[k]));
+    s = __fmaf_ru(g, g, s);
+  }
+  return s;
+}
+
+// Exact reference key (w bits, u << 32 | v) of the edge from query (q, qp) to
+// the point in slot `slot` (mst.py:270-289; bvh.py:284-290).
+template <int D>
+__device__ __forceinline__ void exact_key(const float* q, unsigned qp, const float4* __restrict__ spts, int slot,
+                                          unsigned long long& w, unsigned long long& uv) {
+  const float4 pv = __ldg(spts + slot);
+  const float p[3] = {pv.x, pv.y, pv.z};
+  w = (unsigned long long)__double_as_longlong(exact_dist<D>(q, p));
+  const unsigned pp = __float_as_uint(pv.w);
+  const unsigned long long u = qp < pp ? qp : pp, v = qp < pp ? pp : qp;
+  uv = (u << 32) | v;
+}
+
+// A query's best foreign leaf so far, kept as its slot and an f32 interval
+// [lo, hi] around the squared distance.  The exact f64 weight (the only value
+// that decides acceptance and order) is evaluated once, when the query ends,
+// for all finished lanes of the warp together; the interval alone decides
+// almost every comparison on the way, because two candidates whose intervals
+// are disjoint are separated by >= 1 f32 ulp of d^2 and their f64 weights
+// (error ~2^-52) order the same way.  Overlapping intervals (near-ties) are
+// resolved exactly on the spot.
+struct Pending {
+  int slot;   // -1: none
+  float lo, hi;
+};
+
 // Visit one child of a fetched node record: the f32 lower bound, the component
-// skip (leaves always, mst.py:276; subtrees under subtree_skip, mst.py:291),
-// and for a surviving leaf the exact f64 reference weight (mst.py:270-289).
-// Returns true when an internal child should be explored (lb in *lb_out).
+// skip (leaves always, mst.py:276; subtrees under subtree_skip, mst.py:291) and,
+// for a surviving leaf, the candidate update.  Pruning stays conservative: r2
+// never drops below the squared distance of a real foreign candidate, and a
+// box is pruned only when its lower bound is strictly above r2 (ties at the
+// radius are kept, mst.py:259/282/296).  Returns true when an internal child
+// should be explored (lb in *lb_out).
 template <int D, bool kSkip, bool kBounds, class Rec>
 __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const float* q, unsigned qp, int comp,
-                                            double& radius, float& r2, unsigned long long& best_w,
-                                            unsigned long long& best_uv, const unsigned* __restrict__ perm,
-                                            unsigned long long* ub, unsigned& evals, float* lb_out,
-                                            bool enabled = true) {
+                                            float& r2, Pending& pend, const float4* __restrict__ spts,
+                                            unsigned long long* ub, bool share, unsigned& evals, float* lb_out,
+                                            bool enabled) {
   const int c = side ? rec.ref.y : rec.ref.x;
   const int cl = side ? rec.ref.w : rec.ref.z;
   float lo[3], hi[3];
@@ -109,21 +149,32 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
   if (!enabled || same || lb > r2) return false;
   if (c >= 0) return true;
   ++evals;
-  const double w = exact_dist<D>(q, lo);
-  if (w <= radius) {
-    const unsigned p = __ldg(perm + (~c));
-    const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
-    const unsigned long long uv = (u << 32) | v;
-    const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
-    if (key_less(wb, uv, best_w, best_uv)) {
-      best_w = wb;
-      best_uv = uv;
-      if (w < radius) {
-        radius = w;
-        r2 = prune_r2(w);
-        if (kBounds) atomicMin(&ub[comp], wb);
-      }
+  const float ub2 = point_ub2<D>(q, lo);
+  if (pend.slot < 0 || ub2 < pend.lo) {
+    pend.slot = ~c;   // strictly nearer than the pending candidate (or the first)
+    pend.lo = lb;
+    pend.hi = ub2;
+  } else if (!(lb > pend.hi)) {
+    // overlapping intervals: compare the exact keys
+    unsigned long long wa, uva, wb, uvb;
+    exact_key<D>(q, qp, spts, pend.slot, wa, uva);
+    exact_key<D>(q, qp, spts, ~c, wb, uvb);
+    if (key_less(wb, uvb, wa, uva)) {
+      pend.slot = ~c;
+      pend.lo = lb;
+      pend.hi = ub2;
     }
+  } else {
+    return false;   // strictly farther than the pending candidate
+  }
+  if (pend.hi < r2) {
+    r2 = pend.hi;
+    // Share it with the component's other queries: an upper bound of the
+    // candidate's weight (sqrt rounded up, then 2^-40 slack over any f64
+    // rounding of the exact weight) is at least the weight of a real outgoing
+    // edge, so it is a valid radius for every query of the component.
+    if (kBounds && share)
+      atomicMin(&ub[comp], (unsigned long long)__double_as_longlong(__dmul_ru((double)__fsqrt_ru(pend.hi), 1.0 + 0x1p-40)));
   }
   return false;
 }
@@ -181,39 +232,70 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   double radius = 0.0;
   float r2 = 0.f;
   float my_nlb = 0.f;
-  unsigned long long best_w = ~0ull, best_uv = ~0ull;
+  Pending pend{-1, 0.f, 0.f};
   int top = 0;
   int climb = -1;          // ancestor whose sibling subtree is next, -1 = climb over
   int path_side = 0;       // which child of `climb` the query came from
   int prefix = 0;          // Morton prefix shared by the search box
-  double prefix_r = 0.0;   // radius `prefix` was computed for
+  float prefix_r2 = 0.f;   // r2 `prefix` was computed for
   int since_refresh = 0;
   unsigned evals = 0, visits = 0, found = 0;
-  // a finished query's result waits here until the warp refills, so the
-  // L2-latency CAS of many lanes overlaps instead of stalling the warp per lane
-  bool pend = false;
-  int pcomp = 0;
-  unsigned long long pw = 0, puv = 0;
+  // A finished query keeps its state until the warp refills: the exact weight
+  // of its candidate, the nearest-foreign bound and the 128-bit atomic min then
+  // run for all finished lanes together instead of one divergent lane at a time.
+  bool done = false;
 
-  auto stk_get = [&](int i) -> int2 { return i < kSmemStack ? s_stk[i][tid] : deep[i - kSmemStack]; };
+  auto finalize = [&]() {
+    unsigned long long w = ~0ull, uv = ~0ull;
+    double proven = radius;
+    if (pend.slot >= 0) {
+      exact_key<D>(q, qp, spts, pend.slot, w, uv);
+      const double wd = __longlong_as_double((long long)w);
+      if (wd < proven) proven = wd;
+      // (a strictly smaller radius means another query already beat this edge)
+      if (!(wd > radius)) {
+        ++found;
+        if (singletons) store_key(&best[comp], w, uv);   // round 1: the query is its component
+        else atomic_min_key(&best[comp], w, uv);
+      }
+    }
+    // the search proved: no foreign point closer than `proven`
+    if (kBounds) {
+      const float pr = __double2float_rd(__dmul_rd(proven, 1.0 - 0x1p-40));
+      if (pr > my_nlb) nfn_lb[q0 + s] = pr;
+    }
+    done = false;
+    s = -1;
+  };
+
+  // entry i of this lane's stack is at stk0 + i * kStkStride in the shared window
+  const unsigned stk0 = (unsigned)__cvta_generic_to_shared(&s_stk[0][tid]);
+  constexpr unsigned kStkStride = kTraverseThreads * sizeof(int2);
+  auto stk_get = [&](int i) -> int2 {
+    if (i < kSmemStack) {
+      int2 e;
+      asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(stk0 + i * kStkStride));
+      return e;
+    }
+    return deep[i - kSmemStack];
+  };
   auto stk_put = [&](int i, int node, float lb) {
-    const int2 e = make_int2(node, __float_as_int(lb));
-    if (i < kSmemStack) s_stk[i][tid] = e; else deep[i - kSmemStack] = e;
+    if (i < kSmemStack)
+      asm volatile("st.shared.v2.s32 [%0], {%1, %2};" :: "r"(stk0 + i * kStkStride), "r"(node), "r"(__float_as_int(lb)) : "memory");
+    else
+      deep[i - kSmemStack] = make_int2(node, __float_as_int(lb));
   };
 
   for (;;) {
     // ---- refill idle lanes from the warp's staged chunk of consecutive Morton slots
-    const unsigned idle = __ballot_sync(0xffffffffu, s < 0);
+    const unsigned idle = __ballot_sync(0xffffffffu, s < 0 || done);
     const int n_idle = __popc(idle);
     if (n_idle == 32 && exhausted) {
-      if (pend) atomic_min_key(&best[pcomp], pw, puv);
+      if (done) finalize();
       break;
     }
     if (n_idle >= kRefillIdle) {           // warp-uniform
-      if (pend) {
-        atomic_min_key(&best[pcomp], pw, puv);
-        pend = false;
-      }
+      if (done) finalize();
       if (pool_next >= pool_end && !exhausted) {
         unsigned long long base = 0;
         if (lane == 0) base = atomicAdd(work_counter, (unsigned long long)kTraverseChunk);
@@ -262,14 +344,13 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           comp = s_lab[wib][k];
           radius = kBounds ? bits_to_radius(s_ub[wib][k]) : __longlong_as_double(0x7ff0000000000000ll);
           r2 = prune_r2(radius);
-          best_w = ~0ull;
-          best_uv = ~0ull;
+          pend.slot = -1;
           top = 0;
           const int link = s_lp[wib][k];
           climb = link >> 1;
           path_side = link & 1;
           prefix = radius < 1e300 ? ball_prefix<D>(q, radius, sc) : -1;
-          prefix_r = radius;
+          prefix_r2 = r2;
           since_refresh = kRadiusRefresh / 2;   // staged radius may be stale: refresh early
           my_nlb = kBounds ? s_nlb[wib][k] : 0.f;
           // A previous round proved every foreign point is farther than nfn_lb[s]
@@ -294,12 +375,12 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         }
       }
     }
-    if (s < 0) continue;
+    if (s < 0 || done) continue;
 
-    if (kBounds && ++since_refresh >= kRadiusRefresh) {
+    if (kBounds && !singletons && ++since_refresh >= kRadiusRefresh) {
       since_refresh = 0;
       const double shared = bits_to_radius(__ldcg(&ub[comp]));
-      if (shared < radius) { radius = shared; r2 = prune_r2(shared); }
+      if (shared < radius) { radius = shared; r2 = fminf(r2, prune_r2(shared)); }
     }
     // ---- one node visit per iteration, the same code for both kinds of step so
     // that lanes popping a parked subtree and lanes climbing do not diverge:
@@ -330,10 +411,10 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       int2 u = make_int2(-1, 0);
       if (climbing) u = __ldg(up + node);   // (parent link, prefix length of `climb`)
       float lb0, lb1;
-      const bool w0 = visit_child<D, kSkip, kBounds>(rec, 0, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
-                                                     evals, &lb0, sides & 1u);
-      const bool w1 = visit_child<D, kSkip, kBounds>(rec, 1, q, qp, comp, radius, r2, best_w, best_uv, perm, ub,
-                                                     evals, &lb1, sides & 2u);
+      const bool w0 = visit_child<D, kSkip, kBounds>(rec, 0, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
+                                                     &lb0, sides & 1u);
+      const bool w1 = visit_child<D, kSkip, kBounds>(rec, 1, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
+                                                     &lb1, sides & 2u);
       const bool want0 = w0 && lb0 <= r2, want1 = w1 && lb1 <= r2;
       const int np = (int)want0 + (int)want1;
       if (top + np > kStackCapacity) {
@@ -351,12 +432,14 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         ++top;
       }
       if (climbing && climb >= 0) {
-        // A prefix computed for a larger radius is still a valid (earlier-stopping
-        // is never required) bound; refresh it only when the climb would go on
-        // and the radius has at least halved since.
-        if (u.y > prefix && radius <= 0.5 * prefix_r) {
-          prefix = ball_prefix<D>(q, radius, sc);
-          prefix_r = radius;
+        // Only points with d^2 <= r2 can still matter (anything farther is
+        // beyond the radius or strictly behind the pending candidate).  A prefix
+        // computed for a larger r2 is still valid (earlier stopping is never
+        // required); refresh it when the climb would go on and the search radius
+        // has at least halved since.
+        if (u.y > prefix && r2 <= 0.25f * prefix_r2) {
+          prefix = ball_prefix<D>(q, (double)__fsqrt_ru(r2), sc);
+          prefix_r2 = r2;
         }
         if (u.y <= prefix || u.x < 0) {
           climb = -1;   // every point within the radius lies under this ancestor
@@ -367,24 +450,10 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       }
     }
     if (top == 0 && climb < 0) {
-      // the search proved: no foreign point closer than the final radius
-      if (kBounds) {
-        const float proven = __double2float_rd(radius);
-        if (proven > my_nlb) nfn_lb[q0 + s] = proven;
-      }
-      if (best_uv != ~0ull) {
-        ++found;
-        if (singletons) {
-          store_key(&best[comp], best_w, best_uv);   // round 1: the query is its component
-        } else if (!(__longlong_as_double((long long)best_w) > radius)) {
-          // (a strictly smaller shared radius means another query already beat this edge)
-          pend = true;
-          pcomp = comp;
-          pw = best_w;
-          puv = best_uv;
-        }
-      }
-      s = -1;
+      done = true;
+      // finalize() reads the candidate's point at the next refill: start the
+      // fetch now so that it is an L1 hit by then
+      if (pend.slot >= 0) asm volatile("prefetch.global.L1 [%0];" :: "l"(spts + pend.slot));
     }
   }
   unsigned long long ev64 = evals, vi64 = visits, fo64 = found;
@@ -399,137 +468,6 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     if (vi64) atomicAdd(evals_out + 5, vi64);   // counters[5]: node visits
     if (fo64) atomicAdd(evals_out + 6, fo64);   // counters[6]: queries with a candidate
   }
-}
-
-// ---------------------------------------------------------------------------
-// Warp-packet variant: the 32 lanes of a warp hold 32 consecutive Morton
-// queries and walk ONE shared stack.  A node is visited once per warp (one
-// broadcast 64-byte fetch) and tested by every lane against its own query,
-// radius and component; a child is pushed when any lane still needs it, and
-// each lane keeps its own lower bound per stack entry (NaN = "not for me").
-// Control flow is warp-uniform except the exact f64 leaf test, so SIMT
-// efficiency no longer depends on how different the lanes' path lengths are.
-constexpr int kPacketWarps = kTraverseThreads / 32;
-
-template <int D, bool kSkip, bool kBounds>
-__global__ void __launch_bounds__(kTraverseThreads, 4)
-k_traverse_packet(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
-                  const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
-                  EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
-                  unsigned long long* __restrict__ evals_out, int* __restrict__ overflow) {
-  __shared__ int s_stack[kPacketWarps][kStackCapacity];
-  const unsigned lane = lane_id();
-  const int wib = threadIdx.x >> 5;
-  int* stack_node = s_stack[wib];
-  const long long s = q0 + (blockIdx.x * (long long)kPacketWarps + wib) * 32 + lane;
-  const bool valid = s < q1;
-  if (__ballot_sync(0xffffffffu, valid) == 0) return;
-
-  float q[3] = {0.f, 0.f, 0.f};
-  unsigned qp = 0;
-  int comp = kMixed - 1;   // matches no label
-  double radius = -1.0;
-  float r2 = -1.f;
-  if (valid) {
-    const float4 qv = spts[s];
-    q[0] = qv.x; q[1] = qv.y; q[2] = qv.z;
-    qp = __float_as_uint(qv.w);
-    comp = label[s];
-    radius = kBounds ? bits_to_radius(__ldcg(&ub[comp])) : __longlong_as_double(0x7ff0000000000000ll);
-    r2 = prune_r2(radius);
-  }
-  unsigned long long best_w = ~0ull, best_uv = ~0ull;
-  float stack_lb[kStackCapacity];
-  const float kNone = __int_as_float(0x7fc00000);   // NaN: never <= r2
-  {
-    float rlo[3], rhi[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { rlo[k] = root_box->lo[k]; rhi[k] = root_box->hi[k]; }
-    stack_lb[0] = valid ? box_lb2<D>(q, rlo, rhi) : kNone;
-  }
-  if (lane == 0) stack_node[0] = 0;
-  __syncwarp();
-  int top = 1;
-  int since_refresh = 0;
-  unsigned long long evals = 0;
-
-  while (top > 0) {
-    --top;
-    const int node = stack_node[top];
-    if (kBounds && valid && ++since_refresh >= kRadiusRefresh) {
-      since_refresh = 0;
-      const double shared = bits_to_radius(__ldcg(&ub[comp]));
-      if (shared < radius) { radius = shared; r2 = prune_r2(shared); }
-    }
-    const bool active = stack_lb[top] <= r2;
-    if (!__any_sync(0xffffffffu, active)) continue;
-    const auto rec = load_node(nodes + node);
-    float lbs[2];
-    bool want[2];
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const int c = side ? rec.ref.y : rec.ref.x;
-      const int cl = side ? rec.ref.w : rec.ref.z;
-      float lo[3], hi[3];
-      child_box<D>(rec, side, lo, hi);
-      lbs[side] = box_lb2<D>(q, lo, hi);
-      const bool same = cl == comp && (c < 0 || kSkip);
-      want[side] = active && !same && lbs[side] <= r2;
-      if (c < 0) {   // warp-uniform: leaf child
-        if (want[side]) {
-          ++evals;
-          const double w = exact_dist<D>(q, lo);
-          if (w <= radius) {
-            const unsigned p = __ldg(perm + (~c));
-            const unsigned long long u = qp < p ? qp : p, v = qp < p ? p : qp;
-            const unsigned long long uv = (u << 32) | v;
-            const unsigned long long wb = (unsigned long long)__double_as_longlong(w);
-            if (key_less(wb, uv, best_w, best_uv)) {
-              best_w = wb;
-              best_uv = uv;
-              if (w < radius) {
-                radius = w;
-                r2 = prune_r2(w);
-                if (kBounds) atomicMin(&ub[comp], wb);
-              }
-            }
-          }
-        }
-        want[side] = false;
-      }
-    }
-    const unsigned m0 = __ballot_sync(0xffffffffu, want[0]);
-    const unsigned m1 = __ballot_sync(0xffffffffu, want[1]);
-    const int np = (m0 != 0) + (m1 != 0);
-    if (np == 0) continue;
-    if (top + np > kStackCapacity) {
-      if (lane == 0) atomicOr(overflow, 1);
-      break;
-    }
-    __syncwarp();
-    if (np == 2) {
-      // nearer child on top for the majority of the lanes that need either
-      const unsigned vote = __ballot_sync(0xffffffffu, (want[0] || want[1]) && lbs[1] < lbs[0]);
-      const int near = 2 * __popc(vote) > __popc(m0 | m1) ? 1 : 0;
-      if (lane == 0) {
-        stack_node[top] = near ? rec.ref.x : rec.ref.y;
-        stack_node[top + 1] = near ? rec.ref.y : rec.ref.x;
-      }
-      stack_lb[top] = want[1 - near] ? lbs[1 - near] : kNone;
-      stack_lb[top + 1] = want[near] ? lbs[near] : kNone;
-      top += 2;
-    } else {
-      const int side = m0 ? 0 : 1;
-      if (lane == 0) stack_node[top] = side ? rec.ref.y : rec.ref.x;
-      stack_lb[top] = want[side] ? lbs[side] : kNone;
-      ++top;
-    }
-    __syncwarp();
-  }
-  if (valid && best_uv != ~0ull) atomic_min_key(&best[comp], best_w, best_uv);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
-  if (lane == 0 && evals) atomicAdd(evals_out, evals);
 }
 
 }  // namespace emst
