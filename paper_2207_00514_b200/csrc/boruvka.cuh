@@ -250,8 +250,7 @@ struct MergeScanOp {
   const int* succ;
   const int* root;
   const EdgeKey* best;
-  unsigned* eu;
-  unsigned* ev;
+  unsigned long long* euv;
   unsigned long long* ew;
   long long edge_base;
   int* newid;
@@ -279,8 +278,7 @@ struct MergeScanOp {
       if (v[j] & 1ull) {
         const long long at = edge_base + (long long)(ex & 0x7fffffffull);
         const EdgeKey e = best[k];
-        eu[at] = (unsigned)(e.uv >> 32);
-        ev[at] = (unsigned)(e.uv & 0xffffffffu);
+        euv[at] = e.uv;
         ew[at] = e.w;
       }
       if (v[j] >> 31) newid[k] = (int)(ex >> 31);
@@ -343,25 +341,57 @@ __global__ void k_virtual_reduce(const EdgeKey* __restrict__ shard_keys, int sha
 }
 
 // ------------------------------------------------------------ final output
-__global__ void k_edge_uv_keys(const unsigned* __restrict__ eu, const unsigned* __restrict__ ev, long long ne,
-                               unsigned long long* __restrict__ keys) {
+constexpr int kShortTie = 32;   // tie runs up to this long are ordered in place
+
+// Longest run of equal sorted weights (capped at kShortTie + 1) into *max_run.
+__global__ void k_edge_ties(const unsigned long long* __restrict__ w, long long ne, unsigned* __restrict__ max_run) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < ne) keys[i] = ((unsigned long long)eu[i] << 32) | ev[i];
+  if (i + 1 >= ne || w[i] != w[i + 1] || (i > 0 && w[i - 1] == w[i])) return;   // run starts only
+  unsigned len = 2;
+  while (len <= (unsigned)kShortTie && i + len < ne && w[i + len] == w[i]) ++len;
+  atomicMax(max_run, len);
 }
+
+// Within each run of equal weights (<= kShortTie long), order the edges by
+// (u, v) -- one thread per run, insertion sort (the uv keys are distinct).
+__global__ void k_edge_fix_ties(const unsigned long long* __restrict__ w, long long ne,
+                                const unsigned long long* __restrict__ euv, unsigned* __restrict__ order) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i + 1 >= ne || w[i] != w[i + 1] || (i > 0 && w[i - 1] == w[i])) return;
+  int len = 2;
+  while (len < kShortTie && i + len < ne && w[i + len] == w[i]) ++len;
+  unsigned o[kShortTie];
+  unsigned long long k[kShortTie];
+  for (int a = 0; a < len; ++a) {
+    o[a] = order[i + a];
+    k[a] = euv[o[a]];
+  }
+  for (int a = 1; a < len; ++a) {
+    const unsigned oa = o[a];
+    const unsigned long long ka = k[a];
+    int b = a - 1;
+    while (b >= 0 && k[b] > ka) { k[b + 1] = k[b]; o[b + 1] = o[b]; --b; }
+    k[b + 1] = ka;
+    o[b + 1] = oa;
+  }
+  for (int a = 0; a < len; ++a) order[i + a] = o[a];
+}
+
 __global__ void k_edge_w_keys(const unsigned long long* __restrict__ ew, const unsigned* __restrict__ order, long long ne,
                               unsigned long long* __restrict__ keys) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i < ne) keys[i] = ew[order[i]];
 }
-__global__ void k_edge_emit(const unsigned* __restrict__ eu, const unsigned* __restrict__ ev,
-                            const unsigned long long* __restrict__ ew, const unsigned* __restrict__ order, long long ne,
-                            long long* __restrict__ edges, double* __restrict__ weights) {
+
+// sorted weight bits + edge order -> the reference's int64 (u, v) rows and f64 weights
+__global__ void k_edge_emit(const unsigned long long* __restrict__ w, const unsigned* __restrict__ order,
+                            const unsigned long long* __restrict__ euv, long long ne, long long* __restrict__ edges,
+                            double* __restrict__ weights) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= ne) return;
-  unsigned o = order[i];
-  edges[2 * i] = eu[o];
-  edges[2 * i + 1] = ev[o];
-  weights[i] = __longlong_as_double((long long)ew[o]);
+  const unsigned long long uv = euv[order[i]];
+  reinterpret_cast<longlong2*>(edges)[i] = make_longlong2((long long)(uv >> 32), (long long)(uv & 0xffffffffull));
+  weights[i] = __longlong_as_double((long long)w[i]);
 }
 
 }  // namespace emst

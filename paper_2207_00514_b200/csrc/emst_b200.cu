@@ -112,7 +112,7 @@ struct emst_context {
   DevBuf<unsigned long long> ub;
   DevBuf<EdgeKey> best, shard_keys;
   DevBuf<int> succ, ptr, root, newid, fin;
-  DevBuf<unsigned> eu, ev;
+  DevBuf<unsigned long long> euv;   // emitted edges: u << 32 | v
   DevBuf<unsigned long long> ew;
   DevBuf<unsigned long long> xw, xuv;   // multi-GPU exchange
   DevBuf<unsigned long long> scan_scratch;
@@ -323,8 +323,7 @@ void ensure_rounds(emst_context* c, long long n) {
   c->root.ensure(n);
   c->newid.ensure(n);
   c->fin.ensure(n);
-  c->eu.ensure(n);
-  c->ev.ensure(n);
+  c->euv.ensure(n);
   c->ew.ensure(n);
   if (c->world > 1) {
     c->xw.ensure(n);
@@ -447,7 +446,7 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
          (const unsigned*)c->iperm.p, c->succ.p, err);
   launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
   launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, c->root.p, err);
-  run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->eu.p, c->ev.p, c->ew.p, edge_base, c->newid.p},
+  run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->euv.p, c->ew.p, edge_base, c->newid.p},
            true);
   launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->root.p, (const int*)c->newid.p, comps, c->fin.p);
   launch(c, k_relabel, grid_for(n, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
@@ -460,21 +459,39 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
   return (long long)(tot >> 31);
 }
 
+// Final order (w, u, v) of the n - 1 edges (mst.py:745-747).  One stable radix
+// sort on the weight bits (passes whose digit is constant are skipped); equal
+// weights are then put in (u, v) order: runs of up to kShortTie edges by the
+// thread at the run start, anything longer by the exact two-key LSD sort.
 void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* w_dst) {
   if (ne <= 0) return;
-  launch(c, k_edge_uv_keys, grid_for(ne, 256), 256, 0, (const unsigned*)c->eu.p, (const unsigned*)c->ev.p, ne, c->k0.p);
   unsigned long long* keys;
   unsigned* order;
+  CK(cudaMemcpyAsync(c->k0.p, c->ew.p, ne * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c->stream));
   radix_sort(c, ne, 64, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
-  // second (stable) key: the weight bits, carried in the order of the first sort
-  unsigned long long* kin = keys == c->k0.p ? c->k1.p : c->k0.p;
-  unsigned* vin_alt = order == c->v1.p ? c->v0.p : c->v1.p;
-  launch(c, k_edge_w_keys, grid_for(ne, 256), 256, 0, (const unsigned long long*)c->ew.p, (const unsigned*)order, ne, kin);
-  unsigned long long* keys2;
-  unsigned* order2;
-  radix_sort(c, ne, 64, kin, order, false, keys, vin_alt, &keys2, &order2);
-  launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, (const unsigned*)c->eu.p, (const unsigned*)c->ev.p,
-         (const unsigned long long*)c->ew.p, (const unsigned*)order2, ne, edges_dst, w_dst);
+  long long* tie = dev_counter(c, 7);
+  CK(cudaMemsetAsync(tie, 0, sizeof(long long), c->stream));
+  launch(c, k_edge_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne, (unsigned*)tie);
+  read_counters(c);
+  const unsigned max_run = (unsigned)c->host_counters[7];
+  if (max_run > (unsigned)kShortTie) {
+    // long tie runs: stable sort by (u, v), then stable by w
+    CK(cudaMemcpyAsync(c->k0.p, c->euv.p, ne * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c->stream));
+    radix_sort(c, ne, 64, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
+    unsigned long long* kin = keys == c->k0.p ? c->k1.p : c->k0.p;
+    unsigned* vin_alt = order == c->v1.p ? c->v0.p : c->v1.p;
+    launch(c, k_edge_w_keys, grid_for(ne, 256), 256, 0, (const unsigned long long*)c->ew.p, (const unsigned*)order, ne, kin);
+    unsigned long long* keys2;
+    unsigned* order2;
+    radix_sort(c, ne, 64, kin, order, false, keys, vin_alt, &keys2, &order2);
+    keys = keys2;
+    order = order2;
+  } else if (max_run > 1) {
+    launch(c, k_edge_fix_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne,
+           (const unsigned long long*)c->euv.p, order);
+  }
+  launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, (const unsigned*)order,
+         (const unsigned long long*)c->euv.p, ne, edges_dst, w_dst);
 }
 
 int max_iterations(long long n) {
@@ -648,7 +665,7 @@ int emst_context_destroy(emst_context* c) {
   c->node_parent.release(); c->leaf_parent.release(); c->node_delta.release(); c->up.release(); c->arrivals.release(); c->root_box.release();
   c->label.release(); c->bprefix.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
-  c->eu.release(); c->ev.release(); c->ew.release(); c->xw.release(); c->xuv.release();
+  c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
@@ -1015,13 +1032,11 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
     launch(c, k_cluster_min, grid_for(s, 256), 256, 0, (const int*)c->root.p, (const long long*)dreps.p, s, cmin.p);
     std::vector<int> ptr(s), newlab(n);
     std::vector<long long> cm(s);
-    std::vector<unsigned> eu(emitted), ev(emitted);
-    std::vector<unsigned long long> ew(emitted);
+    std::vector<unsigned long long> euv(emitted), ew(emitted);
     CK(cudaMemcpyAsync(ptr.data(), c->root.p, s * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(cm.data(), cmin.p, s * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     if (emitted) {
-      CK(cudaMemcpyAsync(eu.data(), c->eu.p, emitted * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(ev.data(), c->ev.p, emitted * sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(euv.data(), c->euv.p, emitted * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
       CK(cudaMemcpyAsync(ew.data(), c->ew.p, emitted * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
@@ -1034,8 +1049,8 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
       if (ptr[k] == (int)k) new_reps[nn++] = cm[k];
     std::sort(new_reps, new_reps + nn);
     for (long long e = 0; e < emitted; ++e) {
-      out_u[e] = eu[e];
-      out_v[e] = ev[e];
+      out_u[e] = (long long)(euv[e] >> 32);
+      out_v[e] = (long long)(euv[e] & 0xffffffffull);
       memcpy(&out_w[e], &ew[e], 8);
     }
     *n_edges = emitted;

@@ -69,10 +69,9 @@ __global__ void k_digit_offsets(const unsigned* __restrict__ hist, long long n, 
 struct SortSmem {
   unsigned long long keys[kSortTile];
   unsigned vals[kSortTile];
-  unsigned whist[kSortWarps][kRadix];
+  unsigned short whist[kSortWarps][kRadix];   // per-warp digit counts, then exclusive warp offsets
   unsigned tile_excl[kRadix];
   unsigned long long global_base[kRadix];
-  unsigned scan_tmp[kRadix];
   long long tile;
 };
 
@@ -82,8 +81,33 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
+__device__ __forceinline__ unsigned warp_incl_sum_u32(unsigned v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, v, o);
+    if ((int)(threadIdx.x & 31) >= o) v += t;
+  }
+  return v;
+}
+
+#ifndef EMST_SORT_MINB
+#define EMST_SORT_MINB 3
+#endif
+
+// One counting-sort pass over `shift`'s 8-bit digit.  Per tile of 4096 keys:
+//   1. warp-private stable ranks: the lanes holding the same digit are found
+//      with 8 ballots (one per digit bit); the lowest bumps the warp's counter
+//      in shared memory by the group size and broadcasts the old value (items
+//      are visited in input order, so equal digits keep their input order);
+//   2. per digit: prefix over the warps and the tile total, which is published
+//      at once for the tiles behind;
+//   3. keys and values are staged in shared memory in tile-sorted order (values
+//      are only read here, so the ranking holds just the keys and packed ranks)
+//      -- this is the work that overlaps the predecessors' progress --
+//   4. decoupled look-back for each digit's global start, then the tile is
+//      written out digit-run-contiguous.
 template <bool kIotaValues>
-__global__ void __launch_bounds__(kSortThreads)
+__global__ void __launch_bounds__(kSortThreads, EMST_SORT_MINB)
 k_onesweep(const unsigned long long* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
            unsigned long long* __restrict__ keys_out, unsigned* __restrict__ vals_out, long long n, int shift,
            const unsigned* __restrict__ digit_offset, unsigned* __restrict__ status, unsigned* __restrict__ ticket) {
@@ -91,104 +115,108 @@ k_onesweep(const unsigned long long* __restrict__ keys_in, const unsigned* __res
   SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) sm.tile = (long long)atomicAdd(ticket, 1u);
-  for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&sm.whist[0][0])[i] = 0;
+  for (int i = tid; i < kSortWarps * kRadix / 2; i += kSortThreads) reinterpret_cast<unsigned*>(&sm.whist[0][0])[i] = 0u;
   __syncthreads();
   const long long tile = sm.tile;
   const long long base = tile * kSortTile;
   const long long warp_base = base + warp * (32 * kSortItems);
 
   unsigned long long key[kSortItems];
-  unsigned val[kSortItems];
-  unsigned rank[kSortItems];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    long long i = warp_base + j * 32 + lane;
-    bool ok = i < n;
-    key[j] = ok ? keys_in[i] : ~0ull;
-    if (kIotaValues) val[j] = (unsigned)i;
-    else val[j] = ok ? vals_in[i] : 0u;
+    const long long i = warp_base + j * 32 + lane;
+    key[j] = i < n ? keys_in[i] : ~0ull;
   }
   const unsigned lt = lanemask_lt();
+  unsigned rank2[kSortItems / 2];   // two 16-bit ranks per register
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    long long i = warp_base + j * 32 + lane;
-    bool ok = i < n;
-    unsigned d = ok ? (unsigned)((key[j] >> shift) & (kRadix - 1)) : (unsigned)kRadix;
-    unsigned peers = __match_any_sync(0xffffffffu, d);
+    const long long i = warp_base + j * 32 + lane;
+    const bool ok = i < n;
+    const unsigned d = (unsigned)((key[j] >> shift) & (kRadix - 1));
+    unsigned peers = __ballot_sync(0xffffffffu, ok);
+#pragma unroll
+    for (int b = 0; b < kRadixBits; ++b) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+      peers &= ((d >> b) & 1u) ? bal : ~bal;
+    }
+    const int leader = __ffs(peers) - 1;   // (an invalid lane has peers = 0: leader -1)
     unsigned before = 0;
-    if (ok) before = sm.whist[warp][d];
-    rank[j] = before + __popc(peers & lt);
-    __syncwarp();
-    if (ok && (peers & lt) == 0) sm.whist[warp][d] = before + __popc(peers);
-    __syncwarp();
+    if (ok && lane == leader) {
+      before = sm.whist[warp][d];
+      sm.whist[warp][d] = (unsigned short)(before + __popc(peers));
+    }
+    before = __shfl_sync(0xffffffffu, before, leader < 0 ? 0 : leader);
+    const unsigned r = before + __popc(peers & lt);
+    if (j & 1) rank2[j >> 1] |= r << 16; else rank2[j >> 1] = r;
   }
   __syncthreads();
 
-  // per digit (one thread each): prefix over warps, tile total, look-back
+  // per digit (one thread each): prefix over warps, tile total published
+  const int dg = tid;
+  unsigned total;
   {
-    const int d = tid;
     unsigned run = 0;
 #pragma unroll
     for (int w = 0; w < kSortWarps; ++w) {
-      unsigned c = sm.whist[w][d];
-      sm.whist[w][d] = run;
+      const unsigned c = sm.whist[w][dg];
+      sm.whist[w][dg] = (unsigned short)run;
       run += c;
     }
-    const unsigned total = run;
-    unsigned* my = status + tile * kRadix + d;
-    if (tile == 0) {
-      atomicExch(my, kSortFlagPrefix | total);
-      sm.global_base[d] = digit_offset[d];
-    } else {
-      atomicExch(my, kSortFlagAgg | total);
-      unsigned excl = 0;
-      long long t = tile - 1;
-      for (;;) {
-        unsigned s = *reinterpret_cast<volatile unsigned*>(status + t * kRadix + d);
-        if ((s >> 30) == 0) continue;
-        excl += s & kSortValueMask;
-        if ((s >> 30) == 2) break;
-        --t;
-      }
-      atomicExch(my, kSortFlagPrefix | (excl + total));
-      sm.global_base[d] = (unsigned long long)digit_offset[d] + excl;
+    total = run;
+    atomicExch(status + tile * kRadix + dg, (tile == 0 ? kSortFlagPrefix : kSortFlagAgg) | total);
+    // tile-local exclusive digit starts: block scan of the 256 digit totals
+    const unsigned incl = warp_incl_sum_u32(total);
+    if (lane == 31) sm.tile_excl[warp] = incl;   // (scratch: per-warp sums)
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned ws = lane < kSortWarps ? sm.tile_excl[lane] : 0u;
+      const unsigned wi = warp_incl_sum_u32(ws);
+      if (lane < kSortWarps) sm.tile_excl[lane] = wi - ws;
     }
-    // tile-local exclusive digit starts (block scan over 256 digit totals)
-    sm.scan_tmp[d] = total;
-  }
-  __syncthreads();
-  for (int o = 1; o < kRadix; o <<= 1) {
-    unsigned v = tid >= o ? sm.scan_tmp[tid - o] : 0u;
     __syncthreads();
-    sm.scan_tmp[tid] += v;
+    const unsigned woff = sm.tile_excl[warp];
     __syncthreads();
-  }
-  {
-    unsigned incl = sm.scan_tmp[tid];
-    unsigned tot = incl - (tid > 0 ? sm.scan_tmp[tid - 1] : 0u);
-    __syncthreads();
-    sm.tile_excl[tid] = incl - tot;
+    sm.tile_excl[dg] = woff + incl - total;
   }
   __syncthreads();
 
-  // stage in tile-sorted order
+  // stage keys and values in tile-sorted order
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
-    long long i = warp_base + j * 32 + lane;
+    const long long i = warp_base + j * 32 + lane;
     if (i < n) {
-      unsigned d = (unsigned)((key[j] >> shift) & (kRadix - 1));
-      unsigned pos = sm.tile_excl[d] + sm.whist[warp][d] + rank[j];
+      const unsigned d = (unsigned)((key[j] >> shift) & (kRadix - 1));
+      const unsigned r = (rank2[j >> 1] >> ((j & 1) * 16)) & 0xffffu;
+      const unsigned pos = sm.tile_excl[d] + sm.whist[warp][d] + r;
       sm.keys[pos] = key[j];
-      sm.vals[pos] = val[j];
+      sm.vals[pos] = kIotaValues ? (unsigned)i : vals_in[i];
     }
+  }
+
+  // look-back: global start of this tile's run of each digit
+  if (tile == 0) {
+    sm.global_base[dg] = digit_offset[dg];
+  } else {
+    unsigned excl = 0;
+    long long t = tile - 1;
+    for (;;) {
+      const unsigned s = *reinterpret_cast<volatile unsigned*>(status + t * kRadix + dg);
+      if ((s >> 30) == 0) continue;
+      excl += s & kSortValueMask;
+      if ((s >> 30) == 2) break;
+      --t;
+    }
+    atomicExch(status + tile * kRadix + dg, kSortFlagPrefix | (excl + total));
+    sm.global_base[dg] = (unsigned long long)digit_offset[dg] + excl;
   }
   __syncthreads();
   const long long remain = n - base;
   const int count = remain < kSortTile ? (int)remain : kSortTile;
   for (int i = tid; i < count; i += kSortThreads) {
-    unsigned long long k = sm.keys[i];
-    unsigned d = (unsigned)((k >> shift) & (kRadix - 1));
-    unsigned long long dst = sm.global_base[d] + (unsigned)(i - sm.tile_excl[d]);
+    const unsigned long long k = sm.keys[i];
+    const unsigned d = (unsigned)((k >> shift) & (kRadix - 1));
+    const unsigned long long dst = sm.global_base[d] + (unsigned)(i - sm.tile_excl[d]);
     keys_out[dst] = k;
     vals_out[dst] = sm.vals[i];
   }
