@@ -92,7 +92,15 @@ struct RoundScanOp {
     if (i0 + kScanItems < n) lab[kScanItems] = __ldg(label + i0 + kScanItems);
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) v[j] = (i0 + j + 1 < n && lab[j] != lab[j + 1]) ? 1u : 0u;
+  }
+  // the bound seeding runs after the tile's prefix is out
+  __device__ void side(long long i0, int cnt, const unsigned* v) const {
     if (!bounds) return;   // (warp-uniform)
+    int lab[kScanItems + 1];
+#pragma unroll
+    for (int j = 0; j <= kScanItems; ++j) lab[j] = 0;
+    load8(label, i0, cnt, lab);
+    if (i0 + kScanItems < n) lab[kScanItems] = __ldg(label + i0 + kScanItems);
     unsigned long long wb[kScanItems];
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
@@ -164,6 +172,7 @@ __global__ void k_node_labels(Node* __restrict__ nodes, const int2* __restrict__
 // marks for the next round (each index is read and cleared by one thread).
 struct TopScanOp {
   using T = unsigned;
+  __device__ void side(long long, int, const unsigned*) const {}
   int* mark_lo;
   int* mark_hi;
   int* top;
@@ -247,6 +256,7 @@ __global__ void k_merge_jump(int* ptr, long long c, int* __restrict__ root, int*
 // gives every root its new dense id.
 struct MergeScanOp {
   using T = unsigned long long;
+  __device__ void side(long long, int, const unsigned long long*) const {}
   const int* succ;
   const int* root;
   const EdgeKey* best;

@@ -147,11 +147,18 @@ void read_counters(emst_context* c) {
 // ------------------------------------------------------------------- scan
 template <class Op>
 void run_scan(emst_context* c, long long n, Op op, bool want_total) {
-  long long tiles = scan_tiles(n);
-  c->scan_scratch.ensure(tiles + 1);
-  CK(cudaMemsetAsync(c->scan_scratch.p, 0, (tiles + 1) * sizeof(unsigned long long), c->stream));
+  // one resident block per segment: grid bounded by the occupancy
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan<Op>, kScanThreads, 0));
+  const long long max_blocks = (long long)c->num_sms * std::max(per_sm, 1);
+  const long long tiles = std::max<long long>(1, scan_tiles(n));
+  const long long tiles_per_seg = (tiles + max_blocks - 1) / max_blocks;
+  const long long seg = tiles_per_seg * kScanTile;
+  const long long blocks = std::max<long long>(1, (n + seg - 1) / seg);
+  c->scan_scratch.ensure(blocks);
+  CK(cudaMemsetAsync(c->scan_scratch.p, 0, blocks * sizeof(unsigned long long), c->stream));
   unsigned long long* total = reinterpret_cast<unsigned long long*>(dev_counter(c, 1));
-  launch(c, k_scan<Op>, (unsigned)tiles, kScanThreads, 0, n, c->scan_scratch.p + 1, c->scan_scratch.p, op,
+  launch(c, k_scan<Op>, (unsigned)blocks, kScanThreads, 0, n, seg, c->scan_scratch.p, op,
          want_total ? total : (unsigned long long*)nullptr);
 }
 

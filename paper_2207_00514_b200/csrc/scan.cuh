@@ -11,6 +11,10 @@
 //   Op::T                      the value type (u32, or u64 with 62 value bits)
 //   op.load(i0, cnt, v)        fill v[0..cnt) for items i0.. (side work allowed;
 //                              called by every thread, cnt may be 0)
+//   op.side(i0, cnt, v)        optional work that does not feed the scan, run
+//                              after the tile's prefix is published (so the
+//                              look-back chain of the tiles behind never waits
+//                              on it); called by every thread
 //   op.store(i0, cnt, v, ex)   ex = exclusive prefix of item i0
 // Value arithmetic wraps (mod 2^32 for u32, mod 2^62 for u64), which is exact
 // whenever every true prefix fits, so signed contributions are allowed.
@@ -22,6 +26,7 @@ namespace emst {
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kLookPerLane = 4;   // look-back window = 32 * 4 predecessor tiles
 
 constexpr unsigned long long kFlagAgg = 1ull << 62;
 constexpr unsigned long long kFlagPrefix = 2ull << 62;
@@ -74,22 +79,46 @@ __device__ __forceinline__ T tile_exclusive(T mine, long long tile, unsigned lon
       }
     } else {
       if (tid == 0) st_volatile_u64(&status[tile], pack_status<T>(kFlagAgg, agg));
+      // Look back kLookback tiles per step (lane l reads tiles t-1-4l .. t-4-4l),
+      // so the prefix front advances 128 tiles per round trip instead of 32.
       T excl = T(0);
       long long t = tile - 1;
       for (;;) {
-        const long long idx = t - (long long)tid;
-        unsigned long long st = idx >= 0 ? ld_volatile_u64(&status[idx]) : kFlagPrefix;
-        while (__any_sync(0xffffffffu, (st >> 62) == 0)) {
-          if ((st >> 62) == 0) st = ld_volatile_u64(&status[idx]);
+        unsigned long long st[kLookPerLane];
+#pragma unroll
+        for (int k = 0; k < kLookPerLane; ++k) {
+          const long long idx = t - (long long)tid * kLookPerLane - k;
+          st[k] = idx >= 0 ? ld_volatile_u64(&status[idx]) : kFlagPrefix;
         }
-        const unsigned pm = __ballot_sync(0xffffffffu, (st >> 62) == 2);
+        for (;;) {
+          bool waiting = false;
+#pragma unroll
+          for (int k = 0; k < kLookPerLane; ++k) waiting |= (st[k] >> 62) == 0;
+          if (!__any_sync(0xffffffffu, waiting)) break;
+#pragma unroll
+          for (int k = 0; k < kLookPerLane; ++k) {
+            const long long idx = t - (long long)tid * kLookPerLane - k;
+            if ((st[k] >> 62) == 0) st[k] = ld_volatile_u64(&status[idx]);
+          }
+        }
+        // this lane's sum back to (and including) its nearest inclusive prefix
+        T c = T(0);
+        bool has_prefix = false;
+#pragma unroll
+        for (int k = 0; k < kLookPerLane; ++k) {
+          if (!has_prefix) {
+            c += unpack_status<T>(st[k]);
+            has_prefix = (st[k] >> 62) == 2;
+          }
+        }
+        const unsigned pm = __ballot_sync(0xffffffffu, has_prefix);
         const int stop = pm ? __ffs(pm) - 1 : 31;
-        T c = (int)tid <= stop ? unpack_status<T>(st) : T(0);
+        if ((int)tid > stop) c = T(0);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         excl += c;
         if (pm) break;
-        t -= 32;
+        t -= 32 * kLookPerLane;
       }
       if (tid == 0) {
         st_volatile_u64(&status[tile], pack_status<T>(kFlagPrefix, excl + agg));
@@ -103,30 +132,77 @@ __device__ __forceinline__ T tile_exclusive(T mine, long long tile, unsigned lon
   return s_prefix + s_warp[tid >> 5] + (incl - mine);
 }
 
-// Scratch per scan launch: status[num_tiles] and a ticket counter, zeroed
-// before launch (cudaMemsetAsync of (num_tiles + 1) u64).  The last tile
-// writes the grand total to *total_out when it is given.
+// Block-wide exclusive scan of one value per thread (no look-back); returns the
+// thread's exclusive offset and the block total in *total.
+template <class T>
+__device__ __forceinline__ T block_exclusive(T mine, T* total) {
+  __shared__ T s_w[kScanThreads / 32];
+  __shared__ T s_tot;
+  const int tid = threadIdx.x;
+  const T incl = warp_incl_sum(mine);
+  __syncthreads();   // s_w may still be read from the previous call
+  if (lane_id() == 31) s_w[tid >> 5] = incl;
+  __syncthreads();
+  if (tid < 32) {
+    const T w = tid < kScanThreads / 32 ? s_w[tid] : T(0);
+    const T wi = warp_incl_sum(w);
+    if (tid < kScanThreads / 32) s_w[tid] = wi - w;
+    if (tid == kScanThreads / 32 - 1) s_tot = wi;
+  }
+  __syncthreads();
+  *total = s_tot;
+  return s_w[tid >> 5] + (incl - mine);
+}
+
+// Persistent segmented scan: block b owns the contiguous segment
+// [b * seg, (b + 1) * seg) (seg a multiple of kScanTile) and walks it twice --
+// once to reduce it, once to scan it -- with a single decoupled look-back among
+// the blocks in between (every block is resident, the grid is sized by the
+// occupancy).  The input is read twice, but there is no per-tile serial
+// look-back chain.  status[gridDim.x] must be zeroed before the launch; the
+// grand total goes to *total_out when it is given.
 template <class Op>
 __global__ void __launch_bounds__(kScanThreads)
-k_scan(long long n, unsigned long long* status, unsigned long long* ticket, Op op, unsigned long long* total_out) {
+k_scan(long long n, long long seg, unsigned long long* status, Op op, unsigned long long* total_out) {
   using T = typename Op::T;
-  __shared__ long long s_tile;
-  if (threadIdx.x == 0) s_tile = (long long)atomicAdd(ticket, 1ull);
+  const long long b = blockIdx.x;
+  const long long s0 = b * seg;
+  const long long s1 = min(n, s0 + seg);
+  T acc = T(0);
+  for (long long base = s0; base < s1; base += kScanTile) {
+    const long long i0 = base + (long long)threadIdx.x * kScanItems;
+    const int cnt = i0 >= s1 ? 0 : (s1 - i0 < kScanItems ? (int)(s1 - i0) : kScanItems);
+    T v[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) v[j] = T(0);
+    op.load(i0, cnt, v);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) acc += v[j];
+  }
+  T seg_total;
+  const T my_ex = tile_exclusive<T>(acc, b, status, &seg_total);   // (only its segment prefix is used)
+  __shared__ T s_base;
+  if (threadIdx.x == 0) s_base = my_ex;   // thread 0: exclusive prefix of the whole segment
   __syncthreads();
-  const long long tile = s_tile;
-  const long long i0 = tile * kScanTile + (long long)threadIdx.x * kScanItems;
-  const int cnt = i0 >= n ? 0 : (n - i0 < kScanItems ? (int)(n - i0) : kScanItems);
-  T v[kScanItems];
+  T run = s_base;
+  for (long long base = s0; base < s1; base += kScanTile) {
+    const long long i0 = base + (long long)threadIdx.x * kScanItems;
+    const int cnt = i0 >= s1 ? 0 : (s1 - i0 < kScanItems ? (int)(s1 - i0) : kScanItems);
+    T v[kScanItems];
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) v[j] = T(0);
-  op.load(i0, cnt, v);   // every thread calls it (cnt may be 0): ops may use warp collectives
-  T mine = T(0);
+    for (int j = 0; j < kScanItems; ++j) v[j] = T(0);
+    op.load(i0, cnt, v);
+    T mine = T(0);
 #pragma unroll
-  for (int j = 0; j < kScanItems; ++j) mine += v[j];
-  T total;
-  const T ex = tile_exclusive<T>(mine, tile, status, &total);
-  if (cnt > 0) op.store(i0, cnt, v, ex);
-  if (total_out && threadIdx.x == 0 && (tile + 1) * kScanTile >= n) *total_out = (unsigned long long)total;
+    for (int j = 0; j < kScanItems; ++j) mine += v[j];
+    T tile_total;
+    const T off = block_exclusive<T>(mine, &tile_total);
+    op.side(i0, cnt, v);
+    if (cnt > 0) op.store(i0, cnt, v, run + off);
+    run += tile_total;
+  }
+  if (total_out && threadIdx.x == 0 && s1 >= n && s0 < n) *total_out = (unsigned long long)seg_total;
+  if (total_out && threadIdx.x == 0 && n == 0 && b == 0) *total_out = 0ull;
 }
 
 inline long long scan_tiles(long long n) { return (n + kScanTile - 1) / kScanTile; }
