@@ -165,6 +165,56 @@ __global__ void k_node_labels(Node* __restrict__ nodes, const int2* __restrict__
   }
 }
 
+// Incremental labelling for the subtree-skip traversal.  A pure node stays
+// pure (components only merge), and every query that reaches a node inside a
+// pure subtree came from outside it, i.e. belongs to another component: for
+// such visitors every child inside is foreign.  So when a node is found pure,
+// its child labels become kInside (matches no component) once and for all, and
+// only the nodes that were still mixed need looking at in later rounds.  A
+// mixed node labels its children as before: MIXED, or the current id of a
+// pure child (a top pure node, marked for the top[] scan as in k_node_labels).
+// `list` = the nodes mixed last round (nullptr: all m nodes); the nodes still
+// mixed are appended to out_list (warp-aggregated).
+constexpr int kInside = -2;
+
+template <class Node>
+__global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __restrict__ range,
+                                    const int* __restrict__ bprefix, const int* __restrict__ label,
+                                    const int* __restrict__ list, long long count, int* __restrict__ out_list,
+                                    unsigned* __restrict__ out_count, int* __restrict__ mark_lo,
+                                    int* __restrict__ mark_hi) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool valid = t < count;
+  const int i = valid ? (list ? list[t] : (int)t) : 0;
+  bool mixed = false;
+  if (valid) {
+    const int2 r = range[i];
+    const int2 refs = *reinterpret_cast<const int2*>(&nodes[i].ref.x);
+    const int gamma = refs.x >= 0 ? refs.x : ~refs.x;
+    const int bl = bprefix[r.x], bh = bprefix[r.y];
+    mixed = bl != bh;
+    int2 lab = make_int2(kInside, kInside);
+    if (mixed) {
+      const int bg = bprefix[gamma], bg1 = bprefix[gamma + 1];
+      lab.x = bg == bl ? label[r.x] : kMixed;
+      lab.y = bh == bg1 ? label[r.y] : kMixed;
+      if (mark_lo) {
+        if (refs.x >= 0 && lab.x != kMixed) { mark_lo[r.x] = refs.x + 1; mark_hi[gamma] = refs.x + 1; }
+        if (refs.y >= 0 && lab.y != kMixed) { mark_lo[gamma + 1] = refs.y + 1; mark_hi[r.y] = refs.y + 1; }
+      }
+    }
+    *reinterpret_cast<int2*>(&nodes[i].ref.z) = lab;
+  }
+  const unsigned keep = __ballot_sync(0xffffffffu, mixed);
+  if (keep) {
+    unsigned base = 0;
+    const unsigned lane = threadIdx.x & 31u;
+    if (lane == (unsigned)(__ffs(keep) - 1)) base = atomicAdd(out_count, (unsigned)__popc(keep));
+    base = __shfl_sync(0xffffffffu, base, __ffs(keep) - 1);
+    if (mixed) out_list[base + __popc(keep & ((1u << lane) - 1u))] = i;
+  }
+}
+
 // top[s] = T + 1 for the top pure node T whose range holds slot s, else 0.  The
 // ranges are disjoint, so top[s] = sum_{j <= s} mark_lo[j] - sum_{j < s} mark_hi[j]:
 // an exclusive scan of (mark_lo - mark_hi) plus mark_lo[s], in wrapping u32

@@ -75,6 +75,9 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 
 }  // namespace
 
+constexpr int kCounters = 16;   // [0] evals [1] scan total [2] err [3] overflow [4] work [5] visits
+                                // [6] found [7] ties [8] frontier size
+
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
   bool singleton_round = false;   // every component is one point (round 1 of a solve)
@@ -108,6 +111,10 @@ struct emst_context {
   DevBuf<int> label, bprefix;
   DevBuf<float> nfn_lb;   // per slot: proven lower bound on the nearest-foreign distance
   DevBuf<int> mark_lo, mark_hi, top;   // top pure node per slot (T + 1, 0 = none)
+  DevBuf<int> front[2];                // internal nodes still mixed after the last labelling
+  long long front_n = -1;              // their count (-1: none yet, label every node)
+  bool front_pending = false;
+  int front_cur = 0;
   bool top_valid = false;              // top[] holds this round's values
   DevBuf<unsigned long long> ub;
   DevBuf<EdgeKey> best, shard_keys;
@@ -140,7 +147,7 @@ void launch(emst_context* c, K kernel, unsigned grid, unsigned block, size_t sme
 long long* dev_counter(emst_context* c, int i) { return c->counters.p + i; }
 
 void read_counters(emst_context* c) {
-  CK(cudaMemcpyAsync(c->host_counters, c->counters.p, 8 * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(c->host_counters, c->counters.p, kCounters * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
 }
 
@@ -242,7 +249,7 @@ void ensure_build(emst_context* c, long long n, int d) {
   c->up.ensure(std::max<long long>(n - 1, 1));
   c->arrivals.ensure(std::max<long long>(n - 1, 1));
   c->root_box.ensure(1);
-  c->counters.ensure(8);
+  c->counters.ensure(kCounters);
   c->nodes_stride = node_bytes;
 }
 
@@ -321,6 +328,8 @@ void ensure_rounds(emst_context* c, long long n) {
   c->bprefix.ensure(n);
   c->nfn_lb.ensure(n);
   c->mark_lo.ensure(n);
+  c->front[0].ensure(std::max<long long>(n - 1, 1));
+  c->front[1].ensure(std::max<long long>(n - 1, 1));
   c->mark_hi.ensure(n);
   c->top.ensure(n);
   c->ub.ensure(n);
@@ -344,21 +353,46 @@ __global__ void k_iota_int(int* a, long long n) {
 }
 
 // node labels + upper bounds for the current labels (phases 1-2 of a round)
-void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds,
-                   bool want_top = false) {
-  c->top_valid = false;
+// Node labelling modes for round_prepare
+enum LabelMode {
+  kLabelsFull,       // every node, reference semantics (building blocks, subtree_skip off)
+  kLabelsNone,       // round 1: every child label is still the build's MIXED, and a
+                     // query never reaches its own leaf, so nothing to write
+  kLabelsFrontier,   // only the nodes that were mixed last round (see k_node_labels_front)
+};
+
+template <class Node>
+void launch_labels(emst_context* c, long long n, LabelMode mode, bool want_top) {
+  const long long m = n - 1;
   int* mlo = want_top ? c->mark_lo.p : nullptr;
   int* mhi = want_top ? c->mark_hi.p : nullptr;
+  Node* nodes = reinterpret_cast<Node*>(c->nodes.p);
+  if (mode == kLabelsFull) {
+    launch(c, k_node_labels<Node>, grid_for(m, 256), 256, 0, nodes, (const int2*)c->range.p, (const int*)c->bprefix.p,
+           (const int*)c->label.p, m, mlo, mhi);
+    return;
+  }
+  const long long count = c->front_n < 0 ? m : c->front_n;
+  const int* in = c->front_n < 0 ? nullptr : c->front[c->front_cur].p;
+  int* out = c->front[c->front_cur ^ 1].p;
+  unsigned* out_n = reinterpret_cast<unsigned*>(dev_counter(c, 8));
+  CK(cudaMemsetAsync(out_n, 0, sizeof(long long), c->stream));
+  if (count > 0)
+    launch(c, k_node_labels_front<Node>, grid_for(count, 256), 256, 0, nodes, (const int2*)c->range.p,
+           (const int*)c->bprefix.p, (const int*)c->label.p, in, count, out, out_n, mlo, mhi);
+  c->front_cur ^= 1;
+  c->front_pending = true;   // front_n is read back with the round's counters
+}
+
+void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds,
+                   bool want_top = false, LabelMode mode = kLabelsFull) {
+  c->top_valid = false;
   CK(cudaEventRecord(c->ev_a, c->stream));
   run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds}, false);
   CK(cudaEventRecord(c->ev_b, c->stream));
-  if (n > 1) {
-    if (c->dim == 3)
-      launch(c, k_node_labels<Node3>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node3*>(c->nodes.p),
-             (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1, mlo, mhi);
-    else
-      launch(c, k_node_labels<Node2>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node2*>(c->nodes.p),
-             (const int2*)c->range.p, (const int*)c->bprefix.p, (const int*)c->label.p, n - 1, mlo, mhi);
+  if (n > 1 && mode != kLabelsNone) {
+    if (c->dim == 3) launch_labels<Node3>(c, n, mode, want_top);
+    else launch_labels<Node2>(c, n, mode, want_top);
     if (want_top) {
       run_scan(c, n, TopScanOp{c->mark_lo.p, c->mark_hi.p, c->top.p}, false);
       c->top_valid = true;
@@ -374,6 +408,11 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   CK(cudaEventDestroy(ev_c));
   if (ms_bounds) *ms_bounds += a;
   if (ms_labels) *ms_labels += b;
+  if (c->front_pending) {   // (the sync above made the count readable)
+    read_counters(c);
+    c->front_n = (long long)(unsigned)c->host_counters[8];
+    c->front_pending = false;
+  }
 }
 
 template <int D, bool S, bool B>
@@ -521,10 +560,11 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   build_tree(c, dev_pts, n, d);
   CK(cudaEventRecord(t1, c->stream));
   ensure_rounds(c, n);
-  CK(cudaMemsetAsync(c->counters.p, 0, 8 * sizeof(long long), c->stream));
+  CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
   launch(c, k_iota_int, grid_for(n, 256), 256, 0, c->label.p, n);
   CK(cudaMemsetAsync(c->nfn_lb.p, 0, n * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->mark_lo.p, 0, n * sizeof(int), c->stream));
+  c->front_n = -1;
   CK(cudaMemsetAsync(c->mark_hi.p, 0, n * sizeof(int), c->stream));
   long long comps = n, edges = 0;
   const int max_it = max_iterations(n);
@@ -539,7 +579,11 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     if (st->iterations > max_it) fail(EMST_ERR_ITER, "exceeded the %d-iteration bound for n=%lld", max_it, n);
     CK(cudaMemsetAsync(c->ub.p, 0xff, comps * sizeof(unsigned long long), c->stream));
     CK(cudaMemsetAsync(c->best.p, 0xff, comps * sizeof(EdgeKey), c->stream));
-    round_prepare(c, n, bounds, &ms_labels, &ms_bounds, (flags & EMST_SUBTREE_SKIP) && comps < n);
+    {
+      const bool skip = flags & EMST_SUBTREE_SKIP;
+      const LabelMode mode = comps == n ? kLabelsNone : skip ? kLabelsFrontier : kLabelsFull;
+      round_prepare(c, n, bounds, &ms_labels, &ms_bounds, skip && comps < n, mode);
+    }
     CK(cudaEventRecord(c->ev_a, c->stream));
     c->singleton_round = comps == n;
     c->round = st->iterations;
@@ -642,10 +686,10 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     CK(cudaEventCreate(&c->tv_a));
     CK(cudaEventCreate(&c->tv_b));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-    CK(cudaMallocHost(&c->host_counters, 8 * sizeof(long long)));
+    CK(cudaMallocHost(&c->host_counters, kCounters * sizeof(long long)));
     CK(cudaEventCreate(&c->ev_a));
     CK(cudaEventCreate(&c->ev_b));
-    c->counters.ensure(8);
+    c->counters.ensure(kCounters);
     if (world > 1) {
       if (!nccl_id) fail(EMST_ERR_PARAM, "world > 1 needs an NCCL unique id");
       ncclUniqueId id;
@@ -670,7 +714,8 @@ int emst_context_destroy(emst_context* c) {
   c->sort_hist.release(); c->sort_off.release(); c->sort_status.release(); c->sort_misc.release();
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
   c->node_parent.release(); c->leaf_parent.release(); c->node_delta.release(); c->up.release(); c->arrivals.release(); c->root_box.release();
-  c->label.release(); c->bprefix.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
+  c->label.release(); c->bprefix.release(); c->mark_lo.release(); c->mark_hi.release(); c->top.release();
+  c->front[0].release(); c->front[1].release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release();
@@ -965,7 +1010,7 @@ int emst_find_component_outgoing_edges(emst_context* c, const float* pts, int64_
     // node labels only (bounds are caller-provided)
     round_prepare(c, n, false, nullptr, nullptr);
     CK(cudaMemsetAsync(c->best.p, 0xff, n * sizeof(EdgeKey), c->stream));
-    CK(cudaMemsetAsync(c->counters.p, 0, 8 * sizeof(long long), c->stream));
+    CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
     round_find(c, n, n, flags);
     std::vector<EdgeKey> keys(n);
     CK(cudaMemcpyAsync(keys.data(), c->best.p, n * sizeof(EdgeKey), cudaMemcpyDeviceToHost, c->stream));
@@ -1010,7 +1055,7 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
     if (s < 1 || n < 1) fail(EMST_ERR_PARAM, "empty merge");
     ensure_rounds(c, n);
     c->iperm.ensure(n);
-    c->counters.ensure(8);
+    c->counters.ensure(kCounters);
     std::vector<int> dense(n, -1), lab(n);
     for (long long k = 0; k < s; ++k) dense[reps[k]] = (int)k;
     for (long long i = 0; i < n; ++i) lab[i] = dense[labels[i]];
@@ -1026,7 +1071,7 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
     CK(cudaMemcpyAsync(c->label.p, lab.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->iperm.p, ident.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->best.p, keys.data(), s * sizeof(EdgeKey), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemsetAsync(c->counters.p, 0, 8 * sizeof(long long), c->stream));
+    CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
     long long emitted = 0;
     long long next = round_merge(c, n, s, 0, &emitted);
     if (next >= s) fail(EMST_ERR_NO_REDUCE, "merge did not reduce the component count");
