@@ -266,7 +266,7 @@ def run_ours(args):
                                 "frac": whole_bytes / (ms / 1e3) / 1e9 / (peak * world)},
         "iterations": int(st.iterations), "component_counts": counts,
         "rounds": [{"traverse_ms": round(st.round_traverse_ms[i], 3), "node_visits": int(st.round_node_visits[i]),
-                    "found": int(st.round_found[i])} for i in range(min(st.iterations, 64))],
+                    "found": int(st.round_found[i]), "skipped": int(st.round_skipped[i])} for i in range(min(st.iterations, 64))],
         "phase_ms": {k: round(st.phase_ms[i], 3) for i, k in enumerate(E._lib.PHASES)},
         "clocks": clocks.summary(),
     }

@@ -79,6 +79,7 @@ typedef struct emst_stats {
   double round_traverse_ms[64]; /* per Boruvka round: traversal device time */
   int64_t round_node_visits[64];/* per round: node records fetched by the traversal */
   int64_t round_found[64];      /* per round: queries that found a candidate edge */
+  int64_t round_skipped[64];    /* per round: queries settled before any node visit */
 } emst_stats;
 
 typedef struct emst_context emst_context;

@@ -75,6 +75,7 @@ class Stats(ctypes.Structure):
         ("round_traverse_ms", ctypes.c_double * 64),
         ("round_node_visits", ctypes.c_int64 * 64),
         ("round_found", ctypes.c_int64 * 64),
+        ("round_skipped", ctypes.c_int64 * 64),
     ]
 
 

@@ -76,7 +76,7 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 }  // namespace
 
 constexpr int kCounters = 16;   // [0] evals [1] scan total [2] err [3] overflow [4] work [5] visits
-                                // [6] found [7] ties [8] frontier size
+                                // [6] found [7] ties [8] frontier size [9] skipped queries
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
@@ -571,7 +571,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   st->component_counts[0] = n;
   st->num_counts = 1;
   double ms_labels = 0, ms_bounds = 0, ms_find = 0, ms_merge = 0;
-  long long visits_before = 0, found_before = 0;
+  long long visits_before = 0, found_before = 0, skipped_before = 0;
   double tv_before = c->traverse_ms;
   const bool bounds = flags & EMST_UPPER_BOUNDS;
   while (comps > 1) {
@@ -598,6 +598,8 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
       st->round_traverse_ms[r] = c->traverse_ms - tv_before;
       st->round_node_visits[r] = c->host_counters[5] - visits_before;
       st->round_found[r] = c->host_counters[6] - found_before;
+      st->round_skipped[r] = c->host_counters[9] - skipped_before;
+      skipped_before = c->host_counters[9];
       visits_before = c->host_counters[5];
       found_before = c->host_counters[6];
       tv_before = c->traverse_ms;

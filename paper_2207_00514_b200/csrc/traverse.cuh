@@ -239,7 +239,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   int prefix = 0;          // Morton prefix shared by the search box
   float prefix_r2 = 0.f;   // r2 `prefix` was computed for
   int since_refresh = 0;
-  unsigned evals = 0, visits = 0, found = 0;
+  unsigned evals = 0, visits = 0, found = 0, skipped = 0;
   // A finished query keeps its state until the warp refills: the exact weight
   // of its candidate, the nearest-foreign bound and the 128-bit atomic min then
   // run for all finished lanes together instead of one divergent lane at a time.
@@ -372,6 +372,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
               }
             }
           }
+          skipped += climb < 0;
         }
       }
     }
@@ -456,17 +457,19 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       if (pend.slot >= 0) asm volatile("prefetch.global.L1 [%0];" :: "l"(spts + pend.slot));
     }
   }
-  unsigned long long ev64 = evals, vi64 = visits, fo64 = found;
+  unsigned long long ev64 = evals, vi64 = visits, fo64 = found, sk64 = skipped;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     ev64 += __shfl_xor_sync(0xffffffffu, ev64, o);
     vi64 += __shfl_xor_sync(0xffffffffu, vi64, o);
     fo64 += __shfl_xor_sync(0xffffffffu, fo64, o);
+    sk64 += __shfl_xor_sync(0xffffffffu, sk64, o);
   }
   if (lane == 0) {
     if (ev64) atomicAdd(evals_out, ev64);
     if (vi64) atomicAdd(evals_out + 5, vi64);   // counters[5]: node visits
     if (fo64) atomicAdd(evals_out + 6, fo64);   // counters[6]: queries with a candidate
+    if (sk64) atomicAdd(evals_out + 9, sk64);   // counters[9]: queries settled before any visit
   }
 }
 

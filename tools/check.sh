@@ -10,5 +10,5 @@ for cfg in ${CFGS:-blobs3d_37m}; do
   python -c "
 import json; d=json.loads(open('gpurun_out/bench_$cfg.log').read().strip().splitlines()[-1])
 print('$cfg', round(d['value'],1), 'ms', round(d['ms_per_step'],2), 'trav', round(d['roofline']['ms_per_step'],2), 'e2e', round(d['e2e']['value'],1), d['phase_ms'])
-print([ (round(r['traverse_ms'],2), r['node_visits'], r['found']) for r in d.get('rounds',[])])" || tail -5 gpurun_out/bench_$cfg.log
+print([ (round(r['traverse_ms'],2), r['node_visits'], r['found'], r.get('skipped')) for r in d.get('rounds',[])])" || tail -5 gpurun_out/bench_$cfg.log
 done
