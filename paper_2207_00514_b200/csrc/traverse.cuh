@@ -87,7 +87,13 @@ constexpr int kTraverseThreads = 256;
 constexpr int kTraverseChunk = EMST_TRAV_CHUNK;   // consecutive Morton queries a warp claims at once
 constexpr int kSmemStack = EMST_SMEM_STACK;       // stack entries per lane kept in shared memory
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
-constexpr int kRadiusRefresh = 16;      // pops between re-reads of the shared radius
+constexpr int kRadiusRefresh = 16;
+#ifndef EMST_SHARE_AT_END
+#define EMST_SHARE_AT_END 1
+#endif
+// publish a query's candidate to the component bound when it ends (batched with
+// the other finished lanes) instead of on every improvement
+constexpr bool kShareAtEnd = EMST_SHARE_AT_END;      // pops between re-reads of the shared radius
 
 // f32 upper bound of |q - p|^2 (every operation rounded toward +inf).
 template <int D>
@@ -173,7 +179,7 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
     // candidate's weight (sqrt rounded up, then 2^-40 slack over any f64
     // rounding of the exact weight) is at least the weight of a real outgoing
     // edge, so it is a valid radius for every query of the component.
-    if (kBounds && share)
+    if (kBounds && share && !kShareAtEnd)
       atomicMin(&ub[comp], (unsigned long long)__double_as_longlong(__dmul_ru((double)__fsqrt_ru(pend.hi), 1.0 + 0x1p-40)));
   }
   return false;
@@ -255,8 +261,12 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       // (a strictly smaller radius means another query already beat this edge)
       if (!(wd > radius)) {
         ++found;
-        if (singletons) store_key(&best[comp], w, uv);   // round 1: the query is its component
-        else atomic_min_key(&best[comp], w, uv);
+        if (singletons) {
+          store_key(&best[comp], w, uv);   // round 1: the query is its component
+        } else {
+          if (kBounds && kShareAtEnd && w < __ldcg(&ub[comp])) atomicMin(&ub[comp], w);
+          atomic_min_key(&best[comp], w, uv);
+        }
       }
     }
     // the search proved: no foreign point closer than `proven`
