@@ -80,6 +80,7 @@ typedef struct emst_stats {
   int64_t round_node_visits[64];/* per round: node records fetched by the traversal */
   int64_t round_found[64];      /* per round: queries that found a candidate edge */
   int64_t round_skipped[64];    /* per round: queries settled before any node visit */
+  double total_weight;          /* float(np.sum(weights)): numpy's pairwise order, on the device */
 } emst_stats;
 
 typedef struct emst_context emst_context;

@@ -76,6 +76,7 @@ class Stats(ctypes.Structure):
         ("round_node_visits", ctypes.c_int64 * 64),
         ("round_found", ctypes.c_int64 * 64),
         ("round_skipped", ctypes.c_int64 * 64),
+        ("total_weight", ctypes.c_double),
     ]
 
 

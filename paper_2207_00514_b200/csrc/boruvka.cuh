@@ -454,4 +454,83 @@ __global__ void k_edge_emit(const unsigned long long* __restrict__ w, const unsi
   weights[i] = __longlong_as_double((long long)w[i]);
 }
 
+// ----------------------------------------------------- total weight (numpy order)
+// float(np.sum(weights)) (mst.py:749) reproduced bit for bit: numpy adds a
+// float64 array by pairwise summation -- blocks of <= 128 with 8 interleaved
+// accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus a
+// sequential tail, longer ranges split at n/2 rounded down to a multiple of 8
+// -- and the reduction starts from 0.0 (numpy loops_utils.h.src pairwise_sum).
+// The recursion tree depends on n only, so the 2^L subtrees at depth L are
+// summed by one thread each and their results combined level by level in the
+// same order.  All adds are _rn (no contraction).
+constexpr int kPairwiseLevels = 16;   // up to 65536 partial sums (every node above depth L splits when n >= 256 * 2^L)
+constexpr int kCombineLevels = 12;    // levels one block combines (4096 values in shared memory)
+
+__device__ double pairwise_block(const double* a, long long n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (long long i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = a[j];
+  long long i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+__device__ double pairwise_sum(const double* a, long long n) {
+  if (n <= 128) return pairwise_block(a, n);
+  long long n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_sum(a, n2), pairwise_sum(a + n2, n - n2));
+}
+
+// Subtree `t` at depth `levels` of the split recursion over [0, n): follow the
+// bits of t from the most significant (0 = first half).
+__global__ void k_pairwise_partials(const double* __restrict__ a, long long n, int levels, double* __restrict__ part) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (1 << levels)) return;
+  long long off = 0, len = n;
+  for (int l = levels - 1; l >= 0; --l) {
+    long long n2 = len / 2;
+    n2 -= n2 % 8;
+    if ((t >> l) & 1) { off += n2; len -= n2; } else { len = n2; }
+  }
+  part[t] = pairwise_sum(a + off, len);
+}
+
+// Block b combines the 2^g values part[b * 2^g ..] pairwise, level by level
+// (a depth-g subtree of the recursion), into out[b]; `zero` adds the final 0.0.
+__global__ void k_pairwise_combine(const double* __restrict__ part, int g, double* __restrict__ out, bool zero) {
+  __shared__ double s[1 << kCombineLevels];
+  const double* p = part + ((long long)blockIdx.x << g);
+  for (int i = threadIdx.x; i < (1 << g); i += blockDim.x) s[i] = p[i];
+  __syncthreads();
+  for (int l = g; l > 0; --l) {
+    const int half = 1 << (l - 1);
+    double v[(1 << kCombineLevels) / 2 / 1024];
+#pragma unroll
+    for (int k = 0; k < (1 << kCombineLevels) / 2 / 1024; ++k) {
+      const int i = threadIdx.x + k * 1024;
+      v[k] = i < half ? __dadd_rn(s[2 * i], s[2 * i + 1]) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < (1 << kCombineLevels) / 2 / 1024; ++k) {
+      const int i = threadIdx.x + k * 1024;
+      if (i < half) s[i] = v[k];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = zero ? __dadd_rn(0.0, s[0]) : s[0];
+}
+
 }  // namespace emst

@@ -126,6 +126,7 @@ struct emst_context {
   DevBuf<long long> counters;   // [0] evals, [1] scan total, [2] err, [3] overflow
   DevBuf<long long> out_edges;
   DevBuf<double> out_w;
+  DevBuf<double> pairwise;   // total-weight partial sums
   long long* host_counters = nullptr;   // pinned mirror of `counters`
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   size_t nodes_stride = 0;
@@ -540,6 +541,24 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
          (const unsigned long long*)c->euv.p, ne, edges_dst, w_dst);
 }
 
+// float(np.sum(weights)) on the device in numpy's summation order.
+void total_weight(emst_context* c, const double* w, long long ne, emst_stats* st) {
+  int levels = 0;
+  while (levels < kPairwiseLevels && ne >= (256ll << (levels + 1))) ++levels;
+  c->pairwise.ensure(2 * (1 << kPairwiseLevels) + 1);
+  double* a = c->pairwise.p;
+  double* b = a + (1 << kPairwiseLevels);
+  launch(c, k_pairwise_partials, grid_for(1 << levels, 128), 128, 0, w, ne, levels, a);
+  // combine the recursion tree bottom-up, kCombineLevels levels per launch
+  do {
+    const int g = std::min(levels, kCombineLevels);
+    levels -= g;
+    launch(c, k_pairwise_combine, 1u << levels, 1024, 0, (const double*)a, g, b, levels == 0);
+    std::swap(a, b);
+  } while (levels > 0);
+  CK(cudaMemcpyAsync(&st->total_weight, a, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+}
+
 int max_iterations(long long n) {
   if (n <= 1) return 0;
   int k = 0;
@@ -619,6 +638,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   }
   if (edges != n - 1) fail(EMST_ERR_COUNT, "collected %lld edges for %lld points", edges, n);
   sort_and_emit(c, edges, edges_dev, w_dev);
+  total_weight(c, w_dev, edges, st);
   CK(cudaEventRecord(t2, c->stream));
   CK(cudaEventSynchronize(t2));
   read_counters(c);
@@ -720,7 +740,7 @@ int emst_context_destroy(emst_context* c) {
   c->front[0].release(); c->front[1].release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
-  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release();
+  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);

@@ -220,7 +220,8 @@ def boruvka_emst(points, metric="euclidean", k_pts: int = 1, *, threads: int = 0
     return MstResult(
         edges=edges,
         weights=weights,
-        total_weight=float(np.sum(weights)),
+        # float(np.sum(weights)) (mst.py:749), summed on the device in numpy's pairwise order
+        total_weight=float(st.total_weight) if ne > 0 else 0.0,
         iterations=int(st.iterations),
         phase_timings=timings,
         component_counts=[int(st.component_counts[i]) for i in range(st.num_counts)],

@@ -47,6 +47,7 @@ def test_mst_cases_match_reference(small_golden, skip, bounds):
         assert res.iterations == rec["iterations"], name
         assert res.component_counts == rec["component_counts"], name
         assert res.total_weight == rec["total_weight"], name
+        assert res.total_weight == float(np.sum(res.weights)), name   # device sum in numpy order
 
 
 def test_optimisations_reduce_work(small_golden):
@@ -182,6 +183,7 @@ def test_full_size_configs(large_golden, name):
     assert digest(res.edges, res.weights) == rec["digest"], name
     assert res.iterations == rec["iterations"]
     assert res.component_counts == rec["component_counts"]
+    assert res.total_weight == float(np.sum(res.weights))
     rel = abs(res.total_weight - rec["total_weight"]) / rec["total_weight"]
     assert rel <= 1e-5   # north-star tolerance; bit-equality is asserted through the digest
     # size-independent properties: a spanning tree (n-1 edges, u < v, connected), sorted keys

@@ -40,7 +40,7 @@ def test_library_is_built_for_sm100a():
 
 def test_stats_struct_matches_header():
     # emst_stats layout: field order and sizes must match the C struct
-    assert ctypes.sizeof(_lib.Stats) == 4 + 4 + 64 * 8 + 8 + 8 * 8 + 8 * 4 + 4 + 4 + 8 + 8 + 8 + 4 * 64 * 8
+    assert ctypes.sizeof(_lib.Stats) == 4 + 4 + 64 * 8 + 8 + 8 * 8 + 8 * 4 + 4 + 4 + 8 + 8 + 8 + 4 * 64 * 8 + 8
 
 
 def test_exception_names_match_reference():
