@@ -401,25 +401,31 @@ __global__ void k_virtual_reduce(const EdgeKey* __restrict__ shard_keys, int sha
 }
 
 // ------------------------------------------------------------ final output
-constexpr int kShortTie = 32;   // tie runs up to this long are ordered in place
+constexpr int kShortTie = 32;     // tie runs up to this long are ordered in place by one thread
+constexpr int kBlockTie = 4096;   // longer ones up to this long by one block each
 
-// Longest run of equal sorted weights (capped at kShortTie + 1) into *max_run.
-__global__ void k_edge_ties(const unsigned long long* __restrict__ w, long long ne, unsigned* __restrict__ max_run) {
+// Scan the weight-sorted edges for runs of equal weights: the longest run
+// (capped at kBlockTie + 1) goes to *max_run, and every run longer than
+// kShortTie but at most kBlockTie is appended to `runs` as (start, length).
+__global__ void k_edge_ties(const unsigned long long* __restrict__ w, long long ne, unsigned* __restrict__ max_run,
+                            int2* __restrict__ runs, unsigned* __restrict__ run_count) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i + 1 >= ne || w[i] != w[i + 1] || (i > 0 && w[i - 1] == w[i])) return;   // run starts only
   unsigned len = 2;
-  while (len <= (unsigned)kShortTie && i + len < ne && w[i + len] == w[i]) ++len;
+  while (len <= (unsigned)kBlockTie && i + len < ne && w[i + len] == w[i]) ++len;
   atomicMax(max_run, len);
+  if (len > (unsigned)kShortTie && len <= (unsigned)kBlockTie) runs[atomicAdd(run_count, 1u)] = make_int2((int)i, (int)len);
 }
 
-// Within each run of equal weights (<= kShortTie long), order the edges by
-// (u, v) -- one thread per run, insertion sort (the uv keys are distinct).
+// Within each run of equal weights of at most kShortTie edges, order the edges
+// by (u, v) -- one thread per run, insertion sort (the uv keys are distinct).
 __global__ void k_edge_fix_ties(const unsigned long long* __restrict__ w, long long ne,
                                 const unsigned long long* __restrict__ euv, unsigned* __restrict__ order) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i + 1 >= ne || w[i] != w[i + 1] || (i > 0 && w[i - 1] == w[i])) return;
   int len = 2;
-  while (len < kShortTie && i + len < ne && w[i + len] == w[i]) ++len;
+  while (len <= kShortTie && i + len < ne && w[i + len] == w[i]) ++len;
+  if (len > kShortTie) return;   // a longer run: k_edge_fix_long
   unsigned o[kShortTie];
   unsigned long long k[kShortTie];
   for (int a = 0; a < len; ++a) {
@@ -435,6 +441,41 @@ __global__ void k_edge_fix_ties(const unsigned long long* __restrict__ w, long l
     o[b + 1] = oa;
   }
   for (int a = 0; a < len; ++a) order[i + a] = o[a];
+}
+
+// One block per listed run (kShortTie < length <= kBlockTie): bitonic sort of
+// the run's (uv, edge) pairs in shared memory.
+__global__ void __launch_bounds__(1024) k_edge_fix_long(const int2* __restrict__ runs,
+                                                        const unsigned long long* __restrict__ euv,
+                                                        unsigned* __restrict__ order) {
+  __shared__ unsigned long long sk[kBlockTie];
+  __shared__ unsigned so[kBlockTie];
+  const int2 r = runs[blockIdx.x];
+  int size = 1;
+  while (size < r.y) size <<= 1;
+  for (int a = threadIdx.x; a < size; a += blockDim.x) {
+    const unsigned o = a < r.y ? order[r.x + a] : 0u;
+    so[a] = o;
+    sk[a] = a < r.y ? euv[o] : ~0ull;
+  }
+  __syncthreads();
+  for (int k = 2; k <= size; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int a = threadIdx.x; a < size; a += blockDim.x) {
+        const int b = a ^ j;
+        if (b > a) {
+          const bool up = (a & k) == 0;
+          const unsigned long long ka = sk[a], kb = sk[b];
+          if ((ka > kb) == up) {
+            sk[a] = kb; sk[b] = ka;
+            const unsigned t = so[a]; so[a] = so[b]; so[b] = t;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int a = threadIdx.x; a < r.y; a += blockDim.x) order[r.x + a] = so[a];
 }
 
 __global__ void k_edge_w_keys(const unsigned long long* __restrict__ ew, const unsigned* __restrict__ order, long long ne,

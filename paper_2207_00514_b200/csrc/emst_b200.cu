@@ -127,6 +127,7 @@ struct emst_context {
   DevBuf<long long> out_edges;
   DevBuf<double> out_w;
   DevBuf<double> pairwise;   // total-weight partial sums
+  DevBuf<int2> tie_runs;     // (start, length) of the longer equal-weight runs
   long long* host_counters = nullptr;   // pinned mirror of `counters`
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   size_t nodes_stride = 0;
@@ -516,13 +517,16 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
   unsigned* order;
   CK(cudaMemcpyAsync(c->k0.p, c->ew.p, ne * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c->stream));
   radix_sort(c, ne, 64, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
-  long long* tie = dev_counter(c, 7);
+  long long* tie = dev_counter(c, 7);   // low word: longest run, high word: listed long runs
   CK(cudaMemsetAsync(tie, 0, sizeof(long long), c->stream));
-  launch(c, k_edge_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne, (unsigned*)tie);
+  c->tie_runs.ensure(ne / (kShortTie + 1) + 1);
+  launch(c, k_edge_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne, (unsigned*)tie, c->tie_runs.p,
+         (unsigned*)tie + 1);
   read_counters(c);
-  const unsigned max_run = (unsigned)c->host_counters[7];
-  if (max_run > (unsigned)kShortTie) {
-    // long tie runs: stable sort by (u, v), then stable by w
+  const unsigned max_run = (unsigned)(c->host_counters[7] & 0xffffffffll);
+  const unsigned long_runs = (unsigned)((unsigned long long)c->host_counters[7] >> 32);
+  if (max_run > (unsigned)kBlockTie) {
+    // a very long tie run: exact two-key sort -- stable by (u, v), then stable by w
     CK(cudaMemcpyAsync(c->k0.p, c->euv.p, ne * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c->stream));
     radix_sort(c, ne, 64, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
     unsigned long long* kin = keys == c->k0.p ? c->k1.p : c->k0.p;
@@ -536,6 +540,9 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
   } else if (max_run > 1) {
     launch(c, k_edge_fix_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne,
            (const unsigned long long*)c->euv.p, order);
+    if (long_runs)
+      launch(c, k_edge_fix_long, long_runs, 1024, 0, (const int2*)c->tie_runs.p, (const unsigned long long*)c->euv.p,
+             order);
   }
   launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, (const unsigned*)order,
          (const unsigned long long*)c->euv.p, ne, edges_dst, w_dst);
@@ -740,7 +747,7 @@ int emst_context_destroy(emst_context* c) {
   c->front[0].release(); c->front[1].release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
-  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release();
+  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
