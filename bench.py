@@ -54,6 +54,18 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r01_traverse_traffic.json")
+
+
+def measured_traffic(cfg: str):
+    """DRAM bytes per traversal launch from the committed ncu capture of this config (profiles/), or None."""
+    try:
+        with open(TRAFFIC_PATH) as fh:
+            return float(json.load(fh)[cfg]["dram_bytes_per_launch"])
+    except Exception:
+        return None
+
+
 def algorithmic_bytes(n: int, d: int, counts: list[int]) -> float:
     """(24d+72)n + K(16d+84)n + 56*sum(c_k) + 48(n-1)."""
     rounds = len(counts) - 1
@@ -259,7 +271,11 @@ def run_ours(args):
                 "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": (n - 1) * 24},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_traverse", "achieved": trav_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": trav_gbs / peak, "traffic": None, "peak_source": peak_src,
+                     "frac": trav_gbs / peak, "traffic": measured_traffic(cfg),
+                     "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per k_traverse launch "
+                                       "(profiles/r01_traverse_traffic.json)",
+                     "algorithmic_bytes_per_launch": trav_bytes / max(st.traverse_launches, 1),
+                     "peak_source": peak_src,
                      "bytes_model": f"(12d+36) B per query per round = {12 * d + 36} B",
                      "launches_per_step": st.traverse_launches, "ms_per_step": per_step_trav_ms},
         "whole_step_roofline": {"algorithmic_bytes": whole_bytes, "achieved_gbs": whole_bytes / (ms / 1e3) / 1e9,
