@@ -73,7 +73,7 @@ __device__ __forceinline__ unsigned lanemask_lt_u32() {
 
 constexpr int kTraverseThreads = 256;
 #ifndef EMST_TRAV_MINB
-#define EMST_TRAV_MINB 4
+#define EMST_TRAV_MINB 3
 #endif
 #ifndef EMST_REFILL_IDLE
 #define EMST_REFILL_IDLE 16
@@ -279,7 +279,10 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   };
 
   // entry i of this lane's stack is at stk0 + i * kStkStride in the shared window
-  const unsigned stk0 = (unsigned)__cvta_generic_to_shared(&s_stk[0][tid]);
+  // (kept opaque so that the compiler holds it in one register instead of
+  // re-deriving it from %tid / %cgactaid at every stack access)
+  unsigned stk0;
+  asm volatile("mov.u32 %0, %1;" : "=r"(stk0) : "r"((unsigned)__cvta_generic_to_shared(&s_stk[0][tid])));
   constexpr unsigned kStkStride = kTraverseThreads * sizeof(int2);
   auto stk_get = [&](int i) -> int2 {
     if (i < kSmemStack) {
