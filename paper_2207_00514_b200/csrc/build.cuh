@@ -182,27 +182,27 @@ __global__ void k_pack_up(const int* __restrict__ node_parent, const int* __rest
 }
 
 // --- child box slots inside a node record
+// (child coordinates interleaved: lo[k] at 2k + side, hi[k] at 2D + 2k + side)
 __device__ __forceinline__ void put_child_box(Node3* nodes, int node, int side, const float* lo, const float* hi) {
-  float* f = reinterpret_cast<float*>(&nodes[node]);
-  float* o = f + side * 6;
-  o[0] = lo[0]; o[1] = lo[1]; o[2] = lo[2]; o[3] = hi[0]; o[4] = hi[1]; o[5] = hi[2];
+  float* f = reinterpret_cast<float*>(&nodes[node]) + side;
+  f[0] = lo[0]; f[2] = lo[1]; f[4] = lo[2]; f[6] = hi[0]; f[8] = hi[1]; f[10] = hi[2];
 }
 __device__ __forceinline__ void put_child_box(Node2* nodes, int node, int side, const float* lo, const float* hi) {
-  float4 v = make_float4(lo[0], lo[1], hi[0], hi[1]);
-  if (side == 0) nodes[node].a = v; else nodes[node].b = v;
+  float* f = reinterpret_cast<float*>(&nodes[node]) + side;
+  f[0] = lo[0]; f[2] = lo[1]; f[4] = hi[0]; f[6] = hi[1];
 }
 // L2-coherent read of both child boxes (written by other threads of this launch)
 __device__ __forceinline__ void get_union_box(const Node3* nodes, int node, float* lo, float* hi) {
   const float4* p = reinterpret_cast<const float4*>(&nodes[node]);
   float4 a = __ldcg(p), b = __ldcg(p + 1), c = __ldcg(p + 2);
-  lo[0] = fminf(a.x, b.z); lo[1] = fminf(a.y, b.w); lo[2] = fminf(a.z, c.x);
-  hi[0] = fmaxf(a.w, c.y); hi[1] = fmaxf(b.x, c.z); hi[2] = fmaxf(b.y, c.w);
+  lo[0] = fminf(a.x, a.y); lo[1] = fminf(a.z, a.w); lo[2] = fminf(b.x, b.y);
+  hi[0] = fmaxf(b.z, b.w); hi[1] = fmaxf(c.x, c.y); hi[2] = fmaxf(c.z, c.w);
 }
 __device__ __forceinline__ void get_union_box(const Node2* nodes, int node, float* lo, float* hi) {
   const float4* p = reinterpret_cast<const float4*>(&nodes[node]);
   float4 a = __ldcg(p), b = __ldcg(p + 1);
-  lo[0] = fminf(a.x, b.x); lo[1] = fminf(a.y, b.y);
-  hi[0] = fmaxf(a.z, b.z); hi[1] = fmaxf(a.w, b.w);
+  lo[0] = fminf(a.x, a.y); lo[1] = fminf(a.z, a.w);
+  hi[0] = fmaxf(b.x, b.y); hi[1] = fmaxf(b.z, b.w);
   lo[2] = hi[2] = 0.f;
 }
 
@@ -252,12 +252,11 @@ __global__ void k_export_tree(const Node* __restrict__ nodes, const int* __restr
     int link = node_parent[i];
     int p = link >> 1, side = link & 1;
     const float* f = reinterpret_cast<const float*>(&nodes[p]);
+    const float* o = f + side;   // interleaved children (common.cuh)
     if (sizeof(Node) == sizeof(Node3)) {
-      const float* o = f + side * 6;
-      lo[0] = o[0]; lo[1] = o[1]; lo[2] = o[2]; hi[0] = o[3]; hi[1] = o[4]; hi[2] = o[5];
+      lo[0] = o[0]; lo[1] = o[2]; lo[2] = o[4]; hi[0] = o[6]; hi[1] = o[8]; hi[2] = o[10];
     } else {
-      const float* o = f + side * 4;
-      lo[0] = o[0]; lo[1] = o[1]; hi[0] = o[2]; hi[1] = o[3]; lo[2] = hi[2] = 0.f;
+      lo[0] = o[0]; lo[1] = o[2]; hi[0] = o[4]; hi[1] = o[6]; lo[2] = hi[2] = 0.f;
     }
   }
   for (int k = 0; k < d; ++k) { box_lo[i * d + k] = lo[k]; box_hi[i * d + k] = hi[k]; }

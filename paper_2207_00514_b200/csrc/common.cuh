@@ -17,16 +17,19 @@ constexpr unsigned long long kNoBound = ~0ull;   // "+inf" for u64-bit-pattern m
 
 // One internal node's two children, fetched by a single 64-byte node visit.
 // Leaf children carry their point as a degenerate box, so leaf distances need
-// no second fetch.  Child labels are rewritten every Boruvka round.
+// no second fetch.  Child labels are rewritten every Boruvka round.  The two
+// children's coordinates are interleaved (left, right) so that every pair sits
+// in an aligned register pair and both box tests run as packed f32x2 math:
+// float k of child `side` is lo[k] at 2k + side and hi[k] at 2D + 2k + side.
 struct __align__(16) Node3 {
-  float4 a;   // L.lo.x L.lo.y L.lo.z L.hi.x
-  float4 b;   // L.hi.y L.hi.z R.lo.x R.lo.y
-  float4 c;   // R.lo.z R.hi.x R.hi.y R.hi.z
+  float4 a;   // lo.x L R, lo.y L R
+  float4 b;   // lo.z L R, hi.x L R
+  float4 c;   // hi.y L R, hi.z L R
   int4 ref;   // left ref, right ref, left label, right label
 };
 struct __align__(16) Node2 {
-  float4 a;   // L.lo.x L.lo.y L.hi.x L.hi.y
-  float4 b;   // R.lo.x R.lo.y R.hi.x R.hi.y
+  float4 a;   // lo.x L R, lo.y L R
+  float4 b;   // hi.x L R, hi.y L R
   int4 ref;
 };
 

@@ -29,15 +29,56 @@ namespace emst {
 template <int D>
 __device__ __forceinline__ void child_box(const Node3& rec, int side, float* lo, float* hi) {
   if (side == 0) {
-    lo[0] = rec.a.x; lo[1] = rec.a.y; lo[2] = rec.a.z; hi[0] = rec.a.w; hi[1] = rec.b.x; hi[2] = rec.b.y;
+    lo[0] = rec.a.x; lo[1] = rec.a.z; lo[2] = rec.b.x; hi[0] = rec.b.z; hi[1] = rec.c.x; hi[2] = rec.c.z;
   } else {
-    lo[0] = rec.b.z; lo[1] = rec.b.w; lo[2] = rec.c.x; hi[0] = rec.c.y; hi[1] = rec.c.z; hi[2] = rec.c.w;
+    lo[0] = rec.a.y; lo[1] = rec.a.w; lo[2] = rec.b.y; hi[0] = rec.b.w; hi[1] = rec.c.y; hi[2] = rec.c.w;
   }
 }
 template <int D>
 __device__ __forceinline__ void child_box(const Node2& rec, int side, float* lo, float* hi) {
-  const float4& v = side == 0 ? rec.a : rec.b;
-  lo[0] = v.x; lo[1] = v.y; hi[0] = v.z; hi[1] = v.w; lo[2] = hi[2] = 0.f;
+  if (side == 0) {
+    lo[0] = rec.a.x; lo[1] = rec.a.z; hi[0] = rec.b.x; hi[1] = rec.b.z;
+  } else {
+    lo[0] = rec.a.y; lo[1] = rec.a.w; hi[0] = rec.b.y; hi[1] = rec.b.w;
+  }
+  lo[2] = hi[2] = 0.f;
+}
+
+// Both children's conservative squared lower bounds at once (box_lb2 for each,
+// bit for bit): per axis one packed f32x2 subtraction per face, rounded toward
+// -inf, then max(0, .) per child and a packed fma rounded toward -inf.
+__device__ __forceinline__ unsigned long long f2pack(float x, float y) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(x), "f"(y));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long r, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(r));
+}
+__device__ __forceinline__ void pair_axis(unsigned long long lo, unsigned long long hi, float qk,
+                                          unsigned long long& s) {
+  const unsigned long long q2 = f2pack(qk, qk);
+  unsigned long long a, b, g;
+  asm("sub.rm.f32x2 %0, %1, %2;" : "=l"(a) : "l"(lo), "l"(q2));
+  asm("sub.rm.f32x2 %0, %1, %2;" : "=l"(b) : "l"(q2), "l"(hi));
+  float a0, a1, b0, b1;
+  f2unpack(a, a0, a1);
+  f2unpack(b, b0, b1);
+  g = f2pack(fmaxf(0.f, fmaxf(a0, b0)), fmaxf(0.f, fmaxf(a1, b1)));
+  asm("fma.rm.f32x2 %0, %1, %1, %2;" : "=l"(s) : "l"(g), "l"(s));
+}
+__device__ __forceinline__ void node_lb2(const Node3& r, const float* q, float& lb0, float& lb1) {
+  unsigned long long s = 0ull;   // (+0, +0)
+  pair_axis(f2pack(r.a.x, r.a.y), f2pack(r.b.z, r.b.w), q[0], s);
+  pair_axis(f2pack(r.a.z, r.a.w), f2pack(r.c.x, r.c.y), q[1], s);
+  pair_axis(f2pack(r.b.x, r.b.y), f2pack(r.c.z, r.c.w), q[2], s);
+  f2unpack(s, lb0, lb1);
+}
+__device__ __forceinline__ void node_lb2(const Node2& r, const float* q, float& lb0, float& lb1) {
+  unsigned long long s = 0ull;
+  pair_axis(f2pack(r.a.x, r.a.y), f2pack(r.b.x, r.b.y), q[0], s);
+  pair_axis(f2pack(r.a.z, r.a.w), f2pack(r.b.z, r.b.w), q[1], s);
+  f2unpack(s, lb0, lb1);
 }
 
 // 256-bit read-only loads (LDG.E.ENL2.256 on sm_100a): a 64-byte Node3 is two
@@ -143,18 +184,16 @@ struct Pending {
 template <int D, bool kSkip, bool kBounds, class Rec>
 __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const float* q, unsigned qp, int comp,
                                             float& r2, Pending& pend, const float4* __restrict__ spts,
-                                            unsigned long long* ub, bool share, unsigned& evals, float* lb_out,
+                                            unsigned long long* ub, bool share, unsigned& evals, float lb,
                                             bool enabled) {
   const int c = side ? rec.ref.y : rec.ref.x;
   const int cl = side ? rec.ref.w : rec.ref.z;
-  float lo[3], hi[3];
-  child_box<D>(rec, side, lo, hi);
-  const float lb = box_lb2<D>(q, lo, hi);
-  *lb_out = lb;
   const bool same = cl == comp && (c < 0 || kSkip);
   if (!enabled || same || lb > r2) return false;
   if (c >= 0) return true;
   ++evals;
+  float lo[3], hi[3];
+  child_box<D>(rec, side, lo, hi);
   const float ub2 = point_ub2<D>(q, lo);
   if (pend.slot < 0 || ub2 < pend.lo) {
     pend.slot = ~c;   // strictly nearer than the pending candidate (or the first)
@@ -425,10 +464,11 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       int2 u = make_int2(-1, 0);
       if (climbing) u = __ldg(up + node);   // (parent link, prefix length of `climb`)
       float lb0, lb1;
+      node_lb2(rec, q, lb0, lb1);
       const bool w0 = visit_child<D, kSkip, kBounds>(rec, 0, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
-                                                     &lb0, sides & 1u);
+                                                     lb0, sides & 1u);
       const bool w1 = visit_child<D, kSkip, kBounds>(rec, 1, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
-                                                     &lb1, sides & 2u);
+                                                     lb1, sides & 2u);
       const bool want0 = w0 && lb0 <= r2, want1 = w1 && lb1 <= r2;
       const int np = (int)want0 + (int)want1;
       if (top + np > kStackCapacity) {
