@@ -111,6 +111,19 @@ int emst_context_set_virtual_shards(emst_context* ctx, int shards);
 int emst_boruvka(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags,
                  int64_t* edges_out, double* weights_out, emst_stats* stats, char* err, size_t errlen);
 
+/* boruvka_emst(points, "mrd", k_pts) or boruvka_emst(points, MutualReachability(core)) (mst.py:578-769,
+ * metric.py:128-234): edge weights max(d, core(u), core(v)).  core: NULL to compute the k_pts-th nearest
+ * neighbour distances (self included; 1 <= k_pts <= n, k_pts = 1 is plain Euclidean), or n f64 in
+ * original point order (host).  Outputs as emst_boruvka; stats->phase_ms[EMST_PHASE_CORE] times the cores. */
+int emst_boruvka_mrd(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t k_pts,
+                     const double* core, int64_t* edges_out, double* weights_out, emst_stats* stats, char* err,
+                     size_t errlen);
+
+/* compute_core_distances(build(points), points, k_pts) (metric.py:209-234): core_out n f64 (host), original
+ * point order; k_pts in [1, n] (EMST_ERR_PARAM otherwise). */
+int emst_core_distances(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t k_pts,
+                        double* core_out, char* err, size_t errlen);
+
 /* morton_codes(points) with the tight scene bounds (geometry.py:209-227). codes_out: n u64 (host). */
 int emst_morton_codes(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags,
                       uint64_t* codes_out, char* err, size_t errlen);
@@ -127,14 +140,15 @@ int emst_reduce_labels(emst_context* ctx, const float* pts, int64_t n, int32_t d
 
 /* compute_upper_bounds(state, build(points).leaf_perm, points) (mst.py:451-469): ub_out n f64 by label. */
 int emst_compute_upper_bounds(emst_context* ctx, const float* pts, int64_t n, int32_t d, const int64_t* labels,
-                              double* ub_out, char* err, size_t errlen);
+                              const double* core, double* ub_out, char* err, size_t errlen);
 
 /* find_component_outgoing_edges (mst.py:472-514): per-label best edge arrays (n each, -1 / inf
- * where none), flags as emst_boruvka; ub is read only with EMST_UPPER_BOUNDS. */
+ * where none), flags as emst_boruvka; ub is read only with EMST_UPPER_BOUNDS.  core (both functions):
+ * NULL for Euclidean, else n f64 core distances in point order (mutual reachability). */
 int emst_find_component_outgoing_edges(emst_context* ctx, const float* pts, int64_t n, int32_t d,
-                                       const int64_t* labels, const double* ub, int32_t flags, int64_t* best_u,
-                                       int64_t* best_v, double* best_w, int64_t* leaf_evals, char* err,
-                                       size_t errlen);
+                                       const int64_t* labels, const double* ub, const double* core, int32_t flags,
+                                       int64_t* best_u, int64_t* best_v, double* best_w, int64_t* leaf_evals,
+                                       char* err, size_t errlen);
 
 /* merge_components (mst.py:517-547): reps (s, ascending), per-label best arrays (n); labels
  * (n) relabelled in place; out_u/out_v/out_w (s) and new_reps (s) with their counts. */

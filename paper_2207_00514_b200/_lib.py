@@ -87,6 +87,8 @@ EXPORTS = (
     "emst_context_set_stream",
     "emst_context_set_virtual_shards",
     "emst_boruvka",
+    "emst_boruvka_mrd",
+    "emst_core_distances",
     "emst_morton_codes",
     "emst_build",
     "emst_reduce_labels",
@@ -129,11 +131,13 @@ def load():
         L.emst_context_set_virtual_shards.argtypes = [vp, ctypes.c_int]
         L.emst_context_set_stream.argtypes = [vp, vp]
         L.emst_boruvka.argtypes = [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(Stats), cp, sz]
+        L.emst_boruvka_mrd.argtypes = [vp, vp, i64, i32, i32, i64, vp, vp, vp, ctypes.POINTER(Stats), cp, sz]
+        L.emst_core_distances.argtypes = [vp, vp, i64, i32, i32, i64, vp, cp, sz]
         L.emst_morton_codes.argtypes = [vp, vp, i64, i32, i32, vp, cp, sz]
         L.emst_build.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, cp, sz]
         L.emst_reduce_labels.argtypes = [vp, vp, i64, i32, vp, vp, cp, sz]
-        L.emst_compute_upper_bounds.argtypes = [vp, vp, i64, i32, vp, vp, cp, sz]
-        L.emst_find_component_outgoing_edges.argtypes = [vp, vp, i64, i32, vp, vp, i32, vp, vp, vp, vp, cp, sz]
+        L.emst_compute_upper_bounds.argtypes = [vp, vp, i64, i32, vp, vp, vp, cp, sz]
+        L.emst_find_component_outgoing_edges.argtypes = [vp, vp, i64, i32, vp, vp, vp, i32, vp, vp, vp, vp, cp, sz]
         L.emst_merge_components.argtypes = [vp, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, cp, sz]
         L.emst_build_info.restype = ctypes.c_char_p
         for name in EXPORTS:

@@ -84,6 +84,7 @@ struct RoundScanOp {
   long long n;
   int dim;
   bool bounds;
+  const double* core;   // mutual reachability (slot order), or nullptr
   __device__ void load(long long i0, int cnt, unsigned* v) const {
     int lab[kScanItems + 1];
 #pragma unroll
@@ -108,7 +109,8 @@ struct RoundScanOp {
       if (v[j]) {
         const float4 a = __ldg(spts + i0 + j), b = __ldg(spts + i0 + j + 1);
         const float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
-        const double w = dim == 3 ? exact_dist<3>(pa, pb) : exact_dist<2>(pa, pb);
+        double w = dim == 3 ? exact_dist<3>(pa, pb) : exact_dist<2>(pa, pb);
+        if (core) w = fmax(w, fmax(core[i0 + j], core[i0 + j + 1]));   // mst.py:217-220
         wb[j] = (unsigned long long)__double_as_longlong(w);
       }
     }

@@ -16,6 +16,7 @@
 
 #include "../../include/emst_b200.h"
 #include "boruvka.cuh"
+#include "core.cuh"
 #include "build.cuh"
 #include "radix_sort.cuh"
 #include "scan.cuh"
@@ -112,6 +113,10 @@ struct emst_context {
   DevBuf<float> nfn_lb;   // per slot: proven lower bound on the nearest-foreign distance
   DevBuf<int> mark_lo, mark_hi, top;   // top pure node per slot (T + 1, 0 = none)
   DevBuf<int> front[2];                // internal nodes still mixed after the last labelling
+  // mutual reachability: core distance per slot; `core` points at it while a
+  // mutual-reachability solve / building block runs, nullptr for Euclidean
+  DevBuf<double> core_slot, core_tmp;
+  const double* core = nullptr;
   long long front_n = -1;              // their count (-1: none yet, label every node)
   bool front_pending = false;
   int front_cur = 0;
@@ -390,7 +395,7 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
                    bool want_top = false, LabelMode mode = kLabelsFull) {
   c->top_valid = false;
   CK(cudaEventRecord(c->ev_a, c->stream));
-  run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds}, false);
+  run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds, c->core}, false);
   CK(cudaEventRecord(c->ev_b, c->stream));
   if (n > 1 && mode != kLabelsNone) {
     if (c->dim == 3) launch_labels<Node3>(c, n, mode, want_top);
@@ -417,11 +422,11 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   }
 }
 
-template <int D, bool S, bool B>
-void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
+template <int D, bool S, bool B, bool M>
+void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1) {
   if (q1 <= q0) return;
   using Node = typename NodeOf<D>::type;
-  auto kernel = k_traverse<D, S, B>;
+  auto kernel = k_traverse<D, S, B, M>;
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTraverseThreads, 0));
   const long long warps_needed = (q1 - q0 + kTraverseChunk - 1) / kTraverseChunk;
@@ -437,7 +442,7 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
            reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1,
            c->nfn_lb.p, (const int2*)c->up.p, (const int*)c->leaf_parent.p, (const Scene*)c->scene.p,
-           c->top_valid ? (const int*)c->top.p : (const int*)nullptr);
+           c->top_valid ? (const int*)c->top.p : (const int*)nullptr, c->core);
   }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
@@ -446,6 +451,12 @@ void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
   c->traverse_ms += ms;
   c->traverse_launches++;
   c->traverse_queries += q1 - q0;
+}
+
+template <int D, bool S, bool B>
+void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
+  if (c->core) traverse_range_m<D, S, B, true>(c, out, q0, q1);
+  else traverse_range_m<D, S, B, false>(c, out, q0, q1);
 }
 
 void traverse_dispatch(emst_context* c, int flags, EdgeKey* out, long long q0, long long q1) {
@@ -575,8 +586,61 @@ int max_iterations(long long n) {
 
 // The full solve: build, rounds, final order.  Outputs land in device buffers
 // c->out_edges / c->out_w unless the caller's device pointers are given.
+// ------------------------------------------------------- core distances
+// c->core_slot[s] = core distance of the point in slot s for k_pts (>= 2); the
+// tree must be built.  The per-query heap of k_pts - 1 distances lives in shared
+// memory when it fits in kCoreSmemMax bytes per block, else in global scratch.
+constexpr size_t kCoreSmemMax = 96 * 1024;
+
+template <int D>
+void compute_cores_t(emst_context* c, long long n, long long k_pts) {
+  using Node = typename NodeOf<D>::type;
+  const int kc = (int)(k_pts - 1);
+  const size_t smem = (size_t)kc * kCoreThreads * sizeof(double);
+  const bool in_smem = smem <= kCoreSmemMax;
+  CK(cudaFuncSetAttribute(k_core<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoreSmemMax));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_core<D>, kCoreThreads, in_smem ? smem : 0));
+  const long long blocks_needed = (n + kCoreChunk * (kCoreThreads / 32) - 1) / (kCoreChunk * (kCoreThreads / 32));
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((long long)c->num_sms * std::max(per_sm, 1),
+                                                                             blocks_needed));
+  double* heap = nullptr;
+  if (!in_smem) {
+    c->core_tmp.ensure((size_t)grid * kCoreThreads * kc);
+    heap = c->core_tmp.p;
+  }
+  unsigned long long* work = reinterpret_cast<unsigned long long*>(dev_counter(c, 4));
+  CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
+  launch(c, k_core<D>, grid, kCoreThreads, in_smem ? smem : 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p),
+         (const float4*)c->spts.p, 0ll, n, kc, heap, c->core_slot.p,
+         reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), reinterpret_cast<int*>(dev_counter(c, 3)), work,
+         (const int2*)c->up.p, (const int*)c->leaf_parent.p, (const Scene*)c->scene.p);
+}
+
+// Activate mutual reachability for the current tree: core distances from a
+// caller's table (original point order, host memory) or computed for k_pts.
+// k_pts == 1 without a table is plain Euclidean (all cores 0, mst.py:644).
+void prepare_cores(emst_context* c, long long n, long long k_pts, const double* core_host) {
+  c->core = nullptr;
+  if (!core_host && k_pts <= 1) return;
+  c->core_slot.ensure(n);
+  if (core_host) {
+    c->core_tmp.ensure(n);
+    CK(cudaMemcpyAsync(c->core_tmp.p, core_host, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    launch(c, k_gather_by_perm, grid_for(n, 256), 256, 0, (const double*)c->core_tmp.p, (const unsigned*)c->perm.p, n,
+           c->core_slot.p);
+  } else {
+    if (k_pts > n) fail(EMST_ERR_PARAM, "k_pts must be in [1, %lld], got %lld", n, k_pts);
+    if (c->dim == 3) compute_cores_t<3>(c, n, k_pts);
+    else compute_cores_t<2>(c, n, k_pts);
+    read_counters(c);
+    if (c->host_counters[3]) fail(EMST_ERR_STACK, "neighbour traversal exceeded %d stacked nodes", kStackCapacity);
+  }
+  c->core = c->core_slot.p;
+}
+
 void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags, long long* edges_dev,
-           double* w_dev, emst_stats* st) {
+           double* w_dev, emst_stats* st, long long k_pts = 1, const double* core_host = nullptr) {
   cudaEvent_t t0, t1, t2, t3;
   CK(cudaEventCreate(&t0));
   CK(cudaEventCreate(&t1));
@@ -584,6 +648,9 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   CK(cudaEventCreate(&t3));
   CK(cudaEventRecord(t0, c->stream));
   build_tree(c, dev_pts, n, d);
+  CK(cudaEventRecord(t3, c->stream));
+  CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
+  prepare_cores(c, n, k_pts, core_host);   // (mutual reachability; the "core" phase)
   CK(cudaEventRecord(t1, c->stream));
   ensure_rounds(c, n);
   CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
@@ -658,16 +725,18 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   }
   st->leaf_distance_evals = evals;
   float ms_tree = 0, ms_mst = 0;
-  CK(cudaEventElapsedTime(&ms_tree, t0, t1));
+  float ms_core = 0;
+  CK(cudaEventElapsedTime(&ms_tree, t0, t3));
+  CK(cudaEventElapsedTime(&ms_core, t3, t1));
   CK(cudaEventElapsedTime(&ms_mst, t1, t2));
   st->phase_ms[EMST_PHASE_TREE] = ms_tree;
-  st->phase_ms[EMST_PHASE_CORE] = 0.0;
+  st->phase_ms[EMST_PHASE_CORE] = ms_core;
   st->phase_ms[EMST_PHASE_REDUCE_LABELS] = ms_labels;
   st->phase_ms[EMST_PHASE_UPPER_BOUNDS] = ms_bounds;
   st->phase_ms[EMST_PHASE_FIND_EDGES] = ms_find;
   st->phase_ms[EMST_PHASE_MERGE] = ms_merge;
   st->phase_ms[EMST_PHASE_MST] = ms_mst;
-  st->phase_ms[EMST_PHASE_TOTAL] = ms_tree + ms_mst;
+  st->phase_ms[EMST_PHASE_TOTAL] = ms_tree + ms_core + ms_mst;
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
   cudaEventDestroy(t2);
@@ -744,7 +813,7 @@ int emst_context_destroy(emst_context* c) {
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
   c->node_parent.release(); c->leaf_parent.release(); c->node_delta.release(); c->up.release(); c->arrivals.release(); c->root_box.release();
   c->label.release(); c->bprefix.release(); c->mark_lo.release(); c->mark_hi.release(); c->top.release();
-  c->front[0].release(); c->front[1].release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
+  c->front[0].release(); c->front[1].release(); c->core_slot.release(); c->core_tmp.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release();
@@ -770,8 +839,12 @@ int emst_context_set_virtual_shards(emst_context* c, int shards) {
   return EMST_OK;
 }
 
-int emst_boruvka(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t* edges_out,
-                 double* weights_out, emst_stats* stats, char* err, size_t errlen) {
+}  // extern "C"
+
+namespace {
+int boruvka_impl(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t k_pts,
+                 const double* core_host, int64_t* edges_out, double* weights_out, emst_stats* stats, char* err,
+                 size_t errlen) {
   emst_stats local;
   emst_stats* st = stats ? stats : &local;
   memset(st, 0, sizeof(*st));
@@ -815,7 +888,8 @@ int emst_boruvka(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
       st->component_counts[0] = 1;
       st->num_counts = 1;
     } else {
-      solve(c, dp, n, d, flags, edst, wdst, st);
+      solve(c, dp, n, d, flags, edst, wdst, st, k_pts, core_host);
+      c->core = nullptr;
       if (!(flags & EMST_OUTPUT_ON_DEVICE)) {
         CK(cudaMemcpyAsync(edges_out, edst, 2 * ne * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(weights_out, wdst, ne * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -840,10 +914,63 @@ int emst_boruvka(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
       sscanf(f.msg, "point %lld", &row);
       st->bad_row = row;
     }
-    if (c) cudaStreamSynchronize(c->stream);
+    if (c) {
+      c->core = nullptr;
+      cudaStreamSynchronize(c->stream);
+    }
     return finish(f, err, errlen);
   }
 }
+}  // namespace
+
+extern "C" {
+
+int emst_boruvka(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t* edges_out,
+                 double* weights_out, emst_stats* stats, char* err, size_t errlen) {
+  return boruvka_impl(c, pts, n, d, flags, 1, nullptr, edges_out, weights_out, stats, err, errlen);
+}
+
+int emst_boruvka_mrd(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t k_pts,
+                     const double* core, int64_t* edges_out, double* weights_out, emst_stats* stats, char* err,
+                     size_t errlen) {
+  if (!core && k_pts < 1) {
+    if (err && errlen) snprintf(err, errlen, "k_pts must be >= 1, got %lld", (long long)k_pts);
+    return EMST_ERR_PARAM;
+  }
+  return boruvka_impl(c, pts, n, d, flags, k_pts, core, edges_out, weights_out, stats, err, errlen);
+}
+
+int emst_core_distances(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t k_pts,
+                        double* core_out, char* err, size_t errlen) {
+  try {
+    if (!c) fail(EMST_ERR_PARAM, "null context");
+    set_device(c);
+    check_shape(n, d);
+    if (k_pts < 1 || k_pts > n) fail(EMST_ERR_PARAM, "k_pts must be in [1, %lld], got %lld", (long long)n, (long long)k_pts);
+    if (k_pts == 1) {   // the nearest neighbour counting self is self (metric.py:219-221)
+      memset(core_out, 0, n * sizeof(double));
+      return EMST_OK;
+    }
+    const float* dp = stage_points(c, pts, n, d, flags, nullptr);
+    build_tree(c, dp, n, d);
+    CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
+    prepare_cores(c, n, k_pts, nullptr);
+    c->core = nullptr;
+    c->core_tmp.ensure(n);
+    launch(c, k_scatter_by_perm, grid_for(n, 256), 256, 0, (const double*)c->core_slot.p, (const unsigned*)c->perm.p,
+           n, c->core_tmp.p);
+    CK(cudaMemcpyAsync(core_out, c->core_tmp.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) {
+      c->core = nullptr;
+      cudaStreamSynchronize(c->stream);
+    }
+    return finish(f, err, errlen);
+  }
+}
+
 
 int emst_morton_codes(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, uint64_t* codes_out,
                       char* err, size_t errlen) {
@@ -996,7 +1123,7 @@ int emst_reduce_labels(emst_context* c, const float* pts, int64_t n, int32_t d, 
 }
 
 int emst_compute_upper_bounds(emst_context* c, const float* pts, int64_t n, int32_t d, const int64_t* labels,
-                              double* ub_out, char* err, size_t errlen) {
+                              const double* core, double* ub_out, char* err, size_t errlen) {
   try {
     set_device(c);
     check_shape(n, d);
@@ -1004,7 +1131,9 @@ int emst_compute_upper_bounds(emst_context* c, const float* pts, int64_t n, int3
     build_tree(c, dp, n, d);
     prepare_labels_from_host(c, labels, n);
     CK(cudaMemsetAsync(c->ub.p, 0xff, n * sizeof(unsigned long long), c->stream));
+    prepare_cores(c, n, 1, core);
     round_prepare(c, n, true, nullptr, nullptr);
+    c->core = nullptr;
     std::vector<unsigned long long> bits(n);
     CK(cudaMemcpyAsync(bits.data(), c->ub.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1020,8 +1149,9 @@ int emst_compute_upper_bounds(emst_context* c, const float* pts, int64_t n, int3
 }
 
 int emst_find_component_outgoing_edges(emst_context* c, const float* pts, int64_t n, int32_t d, const int64_t* labels,
-                                       const double* ub, int32_t flags, int64_t* best_u, int64_t* best_v,
-                                       double* best_w, int64_t* leaf_evals, char* err, size_t errlen) {
+                                       const double* ub, const double* core, int32_t flags, int64_t* best_u,
+                                       int64_t* best_v, double* best_w, int64_t* leaf_evals, char* err,
+                                       size_t errlen) {
   try {
     set_device(c);
     check_shape(n, d);
@@ -1040,7 +1170,9 @@ int emst_find_component_outgoing_edges(emst_context* c, const float* pts, int64_
     round_prepare(c, n, false, nullptr, nullptr);
     CK(cudaMemsetAsync(c->best.p, 0xff, n * sizeof(EdgeKey), c->stream));
     CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
+    prepare_cores(c, n, 1, core);
     round_find(c, n, n, flags);
+    c->core = nullptr;
     std::vector<EdgeKey> keys(n);
     CK(cudaMemcpyAsync(keys.data(), c->best.p, n * sizeof(EdgeKey), cudaMemcpyDeviceToHost, c->stream));
     read_counters(c);

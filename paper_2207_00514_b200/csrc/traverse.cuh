@@ -149,13 +149,18 @@ __device__ __forceinline__ float point_ub2(const float* q, const float* p) {
 }
 
 // Exact reference key (w bits, u << 32 | v) of the edge from query (q, qp) to
-// the point in slot `slot` (mst.py:270-289; bvh.py:284-290).
+// the point in slot `slot` (mst.py:270-289; bvh.py:284-290).  With core
+// distances (mutual reachability, slot order) the weight is
+// max(d, core(p), core(q)) (mst.py:278-281).
 template <int D>
 __device__ __forceinline__ void exact_key(const float* q, unsigned qp, const float4* __restrict__ spts, int slot,
-                                          unsigned long long& w, unsigned long long& uv) {
+                                          unsigned long long& w, unsigned long long& uv,
+                                          const double* __restrict__ core = nullptr, double cq = 0.0) {
   const float4 pv = __ldg(spts + slot);
   const float p[3] = {pv.x, pv.y, pv.z};
-  w = (unsigned long long)__double_as_longlong(exact_dist<D>(q, p));
+  double wd = exact_dist<D>(q, p);
+  if (core) wd = fmax(wd, fmax(__ldg(core + slot), cq));
+  w = (unsigned long long)__double_as_longlong(wd);
   const unsigned pp = __float_as_uint(pv.w);
   const unsigned long long u = qp < pp ? qp : pp, v = qp < pp ? pp : qp;
   uv = (u << 32) | v;
@@ -185,7 +190,7 @@ template <int D, bool kSkip, bool kBounds, class Rec>
 __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const float* q, unsigned qp, int comp,
                                             float& r2, Pending& pend, const float4* __restrict__ spts,
                                             unsigned long long* ub, bool share, unsigned& evals, float lb,
-                                            bool enabled) {
+                                            bool enabled, const double* __restrict__ core, double cq) {
   const int c = side ? rec.ref.y : rec.ref.x;
   const int cl = side ? rec.ref.w : rec.ref.z;
   const bool same = cl == comp && (c < 0 || kSkip);
@@ -194,7 +199,14 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
   ++evals;
   float lo[3], hi[3];
   child_box<D>(rec, side, lo, hi);
-  const float ub2 = point_ub2<D>(q, lo);
+  float ub2 = point_ub2<D>(q, lo);
+  if (core) {
+    // mutual reachability: the weight's square lies in [max(lb, cm^2), max(ub2, cm^2)]
+    const double cm = fmax(__ldg(core + ~c), cq);
+    lb = fmaxf(lb, __double2float_rd(__dmul_rd(cm, cm)));
+    ub2 = fmaxf(ub2, __double2float_ru(__dmul_ru(cm, cm)));
+    if (lb > r2) return false;
+  }
   if (pend.slot < 0 || ub2 < pend.lo) {
     pend.slot = ~c;   // strictly nearer than the pending candidate (or the first)
     pend.lo = lb;
@@ -202,8 +214,8 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
   } else if (!(lb > pend.hi)) {
     // overlapping intervals: compare the exact keys
     unsigned long long wa, uva, wb, uvb;
-    exact_key<D>(q, qp, spts, pend.slot, wa, uva);
-    exact_key<D>(q, qp, spts, ~c, wb, uvb);
+    exact_key<D>(q, qp, spts, pend.slot, wa, uva, core, cq);
+    exact_key<D>(q, qp, spts, ~c, wb, uvb, core, cq);
     if (key_less(wb, uvb, wa, uva)) {
       pend.slot = ~c;
       pend.lo = lb;
@@ -238,7 +250,7 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
 // out [depth][thread] (bank = lane for every depth, so lanes at different depths
 // never conflict); deeper entries, rare, spill to a per-thread local array up to
 // the reference's capacity of 64 (bvh.py:36).
-template <int D, bool kSkip, bool kBounds>
+template <int D, bool kSkip, bool kBounds, bool kMrd>
 __global__ void __launch_bounds__(kTraverseThreads, EMST_TRAV_MINB)
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
@@ -246,7 +258,9 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
            unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb,
            const int2* __restrict__ up, const int* __restrict__ leaf_parent, const Scene* __restrict__ scene_ptr,
-           const int* __restrict__ top_pure) {
+           const int* __restrict__ top_pure, const double* __restrict__ core_in) {
+  // mutual reachability (kMrd): core distances per slot; compiled out otherwise
+  const double* __restrict__ core = kMrd ? core_in : nullptr;
   const unsigned lane = lane_id();
   const unsigned lt = lanemask_lt_u32();
   const int total = (int)(q1 - q0);
@@ -277,6 +291,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   double radius = 0.0;
   float r2 = 0.f;
   float my_nlb = 0.f;
+  double cq = 0.0;   // core distance of the query (mutual reachability)
   Pending pend{-1, 0.f, 0.f};
   int top = 0;
   int climb = -1;          // ancestor whose sibling subtree is next, -1 = climb over
@@ -294,7 +309,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     unsigned long long w = ~0ull, uv = ~0ull;
     double proven = radius;
     if (pend.slot >= 0) {
-      exact_key<D>(q, qp, spts, pend.slot, w, uv);
+      exact_key<D>(q, qp, spts, pend.slot, w, uv, core, cq);
       const double wd = __longlong_as_double((long long)w);
       if (wd < proven) proven = wd;
       // (a strictly smaller radius means another query already beat this edge)
@@ -308,8 +323,9 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         }
       }
     }
-    // the search proved: no foreign point closer than `proven`
-    if (kBounds) {
+    // the search proved: no foreign point closer than `proven` (a Euclidean
+    // statement: with core distances the search bounds weights, not distances)
+    if (kBounds && !core) {
       const float pr = __double2float_rd(__dmul_rd(proven, 1.0 - 0x1p-40));
       if (pr > my_nlb) nfn_lb[q0 + s] = pr;
     }
@@ -409,6 +425,11 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           // (foreign sets only shrink, so that stays true).  If that already
           // exceeds the radius, this query cannot find an edge: done.
           if (kBounds && (double)my_nlb > radius) climb = -1;
+          // mutual reachability: every edge of q weighs at least core(q)
+          if (core) {
+            cq = __ldg(core + q0 + s);
+            if (cq > radius) climb = -1;
+          }
           // Every leaf under the query's top pure node T is in its own component:
           // the climb starts above T, and if the search box's prefix already lies
           // inside T there is nothing foreign within the radius at all.
@@ -466,9 +487,9 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       float lb0, lb1;
       node_lb2(rec, q, lb0, lb1);
       const bool w0 = visit_child<D, kSkip, kBounds>(rec, 0, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
-                                                     lb0, sides & 1u);
+                                                     lb0, sides & 1u, core, cq);
       const bool w1 = visit_child<D, kSkip, kBounds>(rec, 1, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
-                                                     lb1, sides & 2u);
+                                                     lb1, sides & 2u, core, cq);
       const bool want0 = w0 && lb0 <= r2, want1 = w1 && lb1 <= r2;
       const int np = (int)want0 + (int)want1;
       if (top + np > kStackCapacity) {

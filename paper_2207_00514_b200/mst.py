@@ -30,6 +30,7 @@ from .errors import (
     NothingToFindError,
 )
 from .geometry import as_point_array
+from .metric import CoreDistances, Euclidean, MutualReachability, core_array, core_pointer
 
 MIXED = -1   # mst.py:57
 
@@ -143,19 +144,19 @@ def _resolve_threads(threads) -> int:
     return 1
 
 
-def _resolve_metric(metric) -> str:
-    """mst.py:562-575; only the Euclidean metric is built for the GPU (SURVEY.md §8f row 1 is next)."""
+def _resolve_metric(metric) -> tuple[str, CoreDistances | None]:
+    """(kind, given core table) as mst.py:562-575."""
     if isinstance(metric, str):
         name = metric.strip().lower().replace("_", "-")
         if name == "euclidean":
-            return "euclidean"
+            return "euclidean", None
         if name in ("mrd", "mutual-reachability"):
-            return "mrd"
+            return "mrd", None
         raise InvalidParameterError(f"metric must be 'euclidean' or 'mrd', got {metric!r}")
-    if type(metric).__name__ == "Euclidean":
-        return "euclidean"
-    if type(metric).__name__ == "MutualReachability":
-        return "mrd"
+    if isinstance(metric, Euclidean):
+        return "euclidean", None
+    if isinstance(metric, MutualReachability):
+        return "mrd", metric.core
     raise InvalidParameterError(f"unknown metric {metric!r}")
 
 
@@ -193,15 +194,20 @@ def boruvka_emst(points, metric="euclidean", k_pts: int = 1, *, threads: int = 0
     k_pts = int(k_pts)
     if k_pts < 1:
         raise InvalidParameterError(f"k_pts must be >= 1, got {k_pts}")
-    kind = _resolve_metric(metric)
+    kind, given_core = _resolve_metric(metric)
     if kind == "euclidean" and k_pts != 1:
         raise InvalidParameterError("k_pts applies to the mrd metric only")
     nthreads = _resolve_threads(threads)
-    if kind == "mrd":
-        raise InvalidParameterError("the mutual-reachability metric is not built for the B200 path yet "
-                                    "(SURVEY.md §8f row 1)")
 
     p, n, d, flags, keep = _device_points(points)
+    core_keep, core_ptr = None, None
+    if kind == "mrd":
+        # mst.py:638-644: a given table (shape-checked by core_array), else k_pts in [1, n]
+        if given_core is not None:
+            core_keep = core_array(MutualReachability(given_core), n)
+            core_ptr = core_keep.ctypes.data
+        elif k_pts > n:
+            raise InvalidParameterError(f"k_pts must be in [1, {n}], got {k_pts}")
     flags |= (_lib.SUBTREE_SKIP if subtree_skip else 0) | (_lib.UPPER_BOUNDS if upper_bound_seeding else 0)
     ne = n - 1
     edges, weights = _host_outputs(max(ne, 1))
@@ -209,8 +215,12 @@ def boruvka_emst(points, metric="euclidean", k_pts: int = 1, *, threads: int = 0
     ctx = context if context is not None else _lib.default_context()
     e = _lib.err_buf()
     with ctx.lock:
-        rc = _lib.load().emst_boruvka(ctx.handle, p, n, d, flags, edges.ctypes.data, weights.ctypes.data,
-                                      ctypes.byref(st), e, len(e))
+        if kind == "mrd":
+            rc = _lib.load().emst_boruvka_mrd(ctx.handle, p, n, d, flags, k_pts, core_ptr, edges.ctypes.data,
+                                              weights.ctypes.data, ctypes.byref(st), e, len(e))
+        else:
+            rc = _lib.load().emst_boruvka(ctx.handle, p, n, d, flags, edges.ctypes.data, weights.ctypes.data,
+                                          ctypes.byref(st), e, len(e))
     _lib.raise_for(rc, e)
     edges = edges[:ne]
     weights = weights[:ne]
@@ -267,11 +277,12 @@ def compute_upper_bounds(state: ComponentState, z_order, points, metric=None) ->
         raise DimensionMismatchError("state, order, and points disagree on size")
     lab = np.ascontiguousarray(state.labels, np.int64)
     ub = np.empty(n, np.float64)
+    core_keep, core_ptr = core_pointer(metric, n)
     ctx = _lib.default_context()
     e = _lib.err_buf()
     with ctx.lock:
         rc = _lib.load().emst_compute_upper_bounds(ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data,
-                                                   ub.ctypes.data, e, len(e))
+                                                   core_ptr, ub.ctypes.data, e, len(e))
     _lib.raise_for(rc, e)
     state.upper_bounds[:] = ub
     return state.upper_bounds
@@ -294,12 +305,13 @@ def find_component_outgoing_edges(bvh: Bvh, points, state: ComponentState, metri
     bw = np.empty(n, np.float64)
     evals = ctypes.c_int64(0)
     flags = (_lib.SUBTREE_SKIP if subtree_skip else 0) | (_lib.UPPER_BOUNDS if use_upper_bounds else 0)
+    core_keep, core_ptr = core_pointer(metric, n)
     ctx = _lib.default_context()
     e = _lib.err_buf()
     with ctx.lock:
         rc = _lib.load().emst_find_component_outgoing_edges(
-            ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data, ub.ctypes.data, flags, bu.ctypes.data,
-            bv.ctypes.data, bw.ctypes.data, ctypes.byref(evals), e, len(e))
+            ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data, ub.ctypes.data, core_ptr, flags,
+            bu.ctypes.data, bv.ctypes.data, bw.ctypes.data, ctypes.byref(evals), e, len(e))
     _lib.raise_for(rc, e)
     missing = reps[bv[reps] < 0]
     if missing.shape[0] > 0:

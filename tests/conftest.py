@@ -33,3 +33,11 @@ def large_golden():
         pytest.skip("large goldens not recorded")
     with open(path) as fh:
         return json.load(fh)
+
+
+@pytest.fixture(scope="session")
+def mrd_golden():
+    arrays = np.load(os.path.join(GOLDEN, "mrd.npz"))
+    with open(os.path.join(GOLDEN, "mrd.json")) as fh:
+        meta = json.load(fh)
+    return arrays, meta

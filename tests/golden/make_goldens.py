@@ -12,6 +12,8 @@ Usage (needs a writable numba cache because the reference tree is read-only)::
     NUMBA_CACHE_DIR=/tmp/numba_cache python tests/golden/make_goldens.py large
 
 ``small`` writes ``tests/golden/small.npz`` + ``tests/golden/small.json`` (seconds);
+``mrd`` writes ``tests/golden/mrd.npz`` + ``tests/golden/mrd.json``: the mutual-reachability
+metric (core distances for k_pts and the MSTs; reference metric.py / mst.py:638-644);
 ``large`` appends the full-size configurations of BASELINE.json to
 ``tests/golden/large.json`` (minutes: 10M-37M points on the host CPU).
 
@@ -263,9 +265,55 @@ def make_large(names=None):
         print(name, rec["iterations"], rec["total_weight"], rec["digest"], f"{dt:.1f}s", flush=True)
 
 
+def make_mrd():
+    """Mutual reachability: core distances and MSTs for k_pts in {2, 4, 16} (criteria 2 and 6)."""
+    emst = _import_reference()
+    arrays, meta = {}, {"cases": {}}
+    cases = []
+    for kind in ("uniform", "normal", "blobs"):
+        for d in (2, 3):
+            for n, seed in ((2, 0), (10, 1), (100, 2), (1000, 3), (5000, 4)):
+                cases.append((kind, n, d, seed))
+    cases.append(("blobs", 20000, 3, 5))
+    cases.append(("blobs", 20000, 2, 6))
+    for kind, n, d, seed in cases:
+        pts = emst.generate(emst.DatasetSpec(kind, n, d, seed=seed))
+        tree = emst.build(pts)
+        name = f"{kind}{d}d_{n}_s{seed}"
+        arrays[name + "/points"] = pts
+        for k in (2, 4, 16):
+            if k > n:
+                continue
+            core = emst.compute_core_distances(tree, pts, k).values
+            res = emst.boruvka_emst(pts, metric="mrd", k_pts=k)
+            key = f"{name}/k{k}"
+            arrays[key + "/core"] = core
+            arrays[key + "/edges"] = res.edges
+            arrays[key + "/weights"] = res.weights
+            rec = _mst_record(res)
+            rec["core_digest"] = array_digest(core.astype("<f8"))
+            meta["cases"][key] = rec
+        print(name, flush=True)
+    # a caller-given core table (MutualReachability(CoreDistances)) that is not a k-NN table
+    pts = emst.generate(emst.DatasetSpec("normal", 3000, 3, seed=7))
+    rng = np.random.default_rng(7)
+    core = rng.random(3000) * 0.3
+    arrays["given/points"] = pts
+    arrays["given/core"] = core
+    res = emst.boruvka_emst(pts, metric=emst.MutualReachability(emst.CoreDistances(4, core)))
+    arrays["given/edges"] = res.edges
+    arrays["given/weights"] = res.weights
+    meta["cases"]["given"] = _mst_record(res)
+    np.savez_compressed(os.path.join(HERE, "mrd.npz"), **arrays)
+    with open(os.path.join(HERE, "mrd.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "small"
     if which == "small":
         make_small()
+    elif which == "mrd":
+        make_mrd()
     else:
         make_large(sys.argv[2:] or None)
