@@ -638,11 +638,138 @@ static double now_s(void) {
 #endif
 }
 
+/* (distance, index) order of the k-NN heap: 1 when entry 1 sorts after entry 2 (metric.py:87-91). */
+static inline int heap_after(double d1, int64_t i1, double d2, int64_t i2) {
+    return d1 > d2 || (d1 == d2 && i1 > i2);
+}
+
+/* Bounded max-heap push (metric.py:94-125); returns the new size. */
+static int64_t heap_push(double *hd, int64_t *hi, int64_t size, int64_t k, double dd, int64_t p) {
+    if (size < k) {
+        int64_t i = size;
+        hd[i] = dd; hi[i] = p;
+        while (i > 0) {
+            int64_t par = (i - 1) >> 1;
+            if (heap_after(hd[i], hi[i], hd[par], hi[par])) {
+                double td = hd[i]; hd[i] = hd[par]; hd[par] = td;
+                int64_t ti = hi[i]; hi[i] = hi[par]; hi[par] = ti;
+                i = par;
+            } else break;
+        }
+        return size + 1;
+    }
+    if (heap_after(hd[0], hi[0], dd, p)) {
+        hd[0] = dd; hi[0] = p;
+        int64_t i = 0;
+        for (;;) {
+            int64_t l = 2 * i + 1, r = l + 1, big = i;
+            if (l < size && heap_after(hd[l], hi[l], hd[big], hi[big])) big = l;
+            if (r < size && heap_after(hd[r], hi[r], hd[big], hi[big])) big = r;
+            if (big == i) break;
+            double td = hd[i]; hd[i] = hd[big]; hd[big] = td;
+            int64_t ti = hi[i]; hi[i] = hi[big]; hi[big] = ti;
+            i = big;
+        }
+    }
+    return size;
+}
+
+/* compute_core_distances (metric.py:128-234): per point the k-th nearest distance counting itself, one
+ * bounded-radius traversal from the root with a (distance, index) max-heap of k entries; boxes at exactly
+ * the radius are still visited.  out indexed by original point; k in [1, n]. */
+static int core_distances(const or_tree *t, const float *pts, int64_t k, double *out) {
+    const int64_t n = t->n, m = t->m;
+    const int d = t->d;
+    if (k == 1) { for (int64_t i = 0; i < n; ++i) out[i] = 0.0; return OR_OK; }
+    int ovf = 0;
+    #pragma omp parallel reduction(| : ovf)
+    {
+        double *hd = (double *)malloc((size_t)k * sizeof(double));
+        int64_t *hi = (int64_t *)malloc((size_t)k * sizeof(int64_t));
+        #pragma omp for schedule(dynamic, 1024)
+        for (int64_t s = 0; s < n; ++s) {
+            int64_t node_stack[OR_STACK];
+            double dist_stack[OR_STACK];
+            double q[3];
+            int64_t qp = t->perm[s];
+            for (int kk = 0; kk < d; ++kk) q[kk] = (double)pts[qp * d + kk];
+            int64_t size = 0;
+            double radius = INFINITY;
+            node_stack[0] = 0;
+            dist_stack[0] = m > 0 ? box_dist(t->box_lo, t->box_hi, d, 0, q) : 0.0;
+            int top = m > 0 ? 1 : 0;
+            if (m == 0) size = heap_push(hd, hi, size, k, 0.0, qp);
+            while (top > 0) {
+                --top;
+                if (dist_stack[top] > radius) continue;
+                int64_t ref = node_stack[top];
+                int64_t child[2] = {t->left[ref], t->right[ref]};
+                int64_t pa = -1, pb = -1;
+                double pa_d = 0.0, pb_d = 0.0;
+                for (int side = 0; side < 2; ++side) {
+                    int64_t c = child[side];
+                    if (c >= m) {
+                        int64_t p = t->perm[c - m];
+                        size = heap_push(hd, hi, size, k, point_dist(pts, d, p, q), p);
+                        if (size == k) radius = hd[0];
+                    } else {
+                        double bd = box_dist(t->box_lo, t->box_hi, d, c, q);
+                        if (bd <= radius) {
+                            if (pa < 0) { pa = c; pa_d = bd; }
+                            else { pb = c; pb_d = bd; }
+                        }
+                    }
+                }
+                if (pb >= 0) {
+                    if (top + 2 > OR_STACK) { ovf = 1; top = 0; continue; }
+                    if (pb_d < pa_d) {
+                        int64_t tn = pa; pa = pb; pb = tn;
+                        double td = pa_d; pa_d = pb_d; pb_d = td;
+                    }
+                    node_stack[top] = pb; dist_stack[top] = pb_d; ++top;
+                    node_stack[top] = pa; dist_stack[top] = pa_d; ++top;
+                } else if (pa >= 0) {
+                    if (top + 1 > OR_STACK) { ovf = 1; top = 0; continue; }
+                    node_stack[top] = pa; dist_stack[top] = pa_d; ++top;
+                }
+            }
+            out[qp] = hd[0];
+        }
+        free(hd);
+        free(hi);
+    }
+    return ovf ? OR_ERR_STACK : OR_OK;
+}
+
+int oracle_core_distances(const float *pts, int64_t n, int d, int64_t k, double *out) {
+    or_tree t;
+    int rc = tree_build(&t, pts, n, d);
+    if (rc) return rc;
+    rc = core_distances(&t, pts, k, out);
+    tree_free(&t);
+    return rc;
+}
+
 /* boruvka_emst / _run_boruvka, Euclidean metric (mst.py:578-769).
  * flags bit0 subtree_skip, bit1 upper_bound_seeding.  edges_out (n-1)x2 int64,
  * weights_out (n-1) float64, sorted by (w, u, v). */
+static int boruvka(const float *pts, int64_t n, int d, int flags, int64_t k_pts, const double *given_cores,
+                   int64_t *edges_out, double *weights_out, oracle_stats *st);
+
 int oracle_boruvka(const float *pts, int64_t n, int d, int flags, int64_t *edges_out, double *weights_out,
                    oracle_stats *st) {
+    return boruvka(pts, n, d, flags, 1, NULL, edges_out, weights_out, st);
+}
+
+/* boruvka_emst(points, "mrd", k_pts) / MutualReachability(core) (mst.py:638-644): given_cores (original
+ * order) or NULL to compute them for k_pts (k_pts = 1 without a table is the Euclidean metric). */
+int oracle_boruvka_mrd(const float *pts, int64_t n, int d, int flags, int64_t k_pts, const double *given_cores,
+                       int64_t *edges_out, double *weights_out, oracle_stats *st) {
+    return boruvka(pts, n, d, flags, k_pts, given_cores, edges_out, weights_out, st);
+}
+
+static int boruvka(const float *pts, int64_t n, int d, int flags, int64_t k_pts, const double *given_cores,
+                   int64_t *edges_out, double *weights_out, oracle_stats *st) {
     const int skip = flags & 1, use_bounds = (flags >> 1) & 1;
     double t_start = now_s();
     memset(st, 0, sizeof(*st));
@@ -650,6 +777,15 @@ int oracle_boruvka(const float *pts, int64_t n, int d, int flags, int64_t *edges
     int rc = tree_build(&t, pts, n, d);
     if (rc) return rc;
     double t_tree = now_s() - t_start;
+    double tc = now_s();
+    double *cores = NULL;
+    if (given_cores || k_pts > 1) {
+        cores = (double *)malloc((size_t)n * sizeof(double));
+        if (!cores) { tree_free(&t); return OR_ERR_ALLOC; }
+        if (given_cores) memcpy(cores, given_cores, (size_t)n * sizeof(double));
+        else if ((rc = core_distances(&t, pts, k_pts, cores))) { free(cores); tree_free(&t); return rc; }
+    }
+    double t_core = now_s() - tc;
     double t0 = now_s();
     int64_t m = n - 1;
     int64_t *labels = (int64_t *)malloc((size_t)n * sizeof(int64_t));
@@ -691,12 +827,12 @@ int oracle_boruvka(const float *pts, int64_t n, int d, int flags, int64_t *edges
         t1 = now_s();
         if (use_bounds) {
             for (int64_t i = 0; i < nreps; ++i) ub[reps[i]] = INFINITY;
-            upper_bounds(pts, d, t.perm, n, labels, NULL, ub);
+            upper_bounds(pts, d, t.perm, n, labels, cores, ub);
         }
         t_bounds += now_s() - t1;
         t1 = now_s();
         int ovf = 0;
-        st->leaf_distance_evals += find_edges(&t, pts, labels, il, ub, NULL, use_bounds, skip, 0, n,
+        st->leaf_distance_evals += find_edges(&t, pts, labels, il, ub, cores, use_bounds, skip, 0, n,
                                               cu, cv, cw, &ovf);
         if (ovf) { rc = OR_ERR_STACK; goto done; }
         for (int64_t i = 0; i < nreps; ++i) { bu[reps[i]] = -1; bv[reps[i]] = -1; bw[reps[i]] = INFINITY; }
@@ -726,7 +862,7 @@ int oracle_boruvka(const float *pts, int64_t n, int d, int flags, int64_t *edges
         weights_out[i] = ew[order[i]];
     }
     st->phase_seconds[0] = t_tree;
-    st->phase_seconds[1] = 0.0;
+    st->phase_seconds[1] = t_core;
     st->phase_seconds[2] = t_reduce;
     st->phase_seconds[3] = t_bounds;
     st->phase_seconds[4] = t_find;
@@ -736,6 +872,7 @@ int oracle_boruvka(const float *pts, int64_t n, int d, int flags, int64_t *edges
 done:
     free(labels); free(il); free(ub); free(reps); free(cu); free(cv); free(cw); free(bu); free(bv); free(bw);
     free(succ); free(term); free(cmin); free(fin); free(new_reps); free(eu); free(ev); free(ew); free(order);
+    free(cores);
     tree_free(&t);
     return rc;
 }

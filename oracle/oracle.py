@@ -78,6 +78,9 @@ def lib():
         L.oracle_merge.argtypes = [i64, _i64p, i64, _i64p, _i64p, _f64p, _i64p, _i64p, _i64p, _f64p,
                                    ctypes.POINTER(ctypes.c_int64), _i64p, ctypes.POINTER(ctypes.c_int64)]
         L.oracle_boruvka.argtypes = [_f32p, i64, i32, i32, _i64p, _f64p, ctypes.POINTER(_Stats)]
+        L.oracle_boruvka_mrd.argtypes = [_f32p, i64, i32, i32, i64, ctypes.c_void_p, _i64p, _f64p,
+                                         ctypes.POINTER(_Stats)]
+        L.oracle_core_distances.argtypes = [_f32p, i64, i32, i64, _f64p]
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -205,15 +208,31 @@ class OracleResult:
 PHASES = ("tree", "core", "reduce_labels", "upper_bounds", "find_edges", "merge", "mst", "total")
 
 
-def boruvka_emst(points, *, subtree_skip=True, upper_bound_seeding=True) -> OracleResult:
-    """The reference's boruvka_emst (mst.py:578-769), Euclidean metric."""
+def core_distances(points, k_pts: int) -> np.ndarray:
+    """compute_core_distances (metric.py:128-234): k_pts-th nearest distance counting self, by point."""
+    p = _pts(points)
+    n, d = p.shape
+    out = np.empty(n, np.float64)
+    _check(lib().oracle_core_distances(p, n, d, int(k_pts), out))
+    return out
+
+
+def boruvka_emst(points, *, subtree_skip=True, upper_bound_seeding=True, k_pts: int = 1,
+                 cores=None) -> OracleResult:
+    """The reference's boruvka_emst (mst.py:578-769): Euclidean, or mutual reachability when k_pts > 1
+    (cores computed as compute_core_distances) or a core table is given (MutualReachability)."""
     p = _pts(points)
     n, d = p.shape
     edges = np.empty((max(n - 1, 1), 2), np.int64)
     weights = np.empty(max(n - 1, 1), np.float64)
     st = _Stats()
     flags = (1 if subtree_skip else 0) | (2 if upper_bound_seeding else 0)
-    _check(lib().oracle_boruvka(p, n, d, flags, edges.reshape(-1), weights, ctypes.byref(st)))
+    if cores is None and k_pts == 1:
+        _check(lib().oracle_boruvka(p, n, d, flags, edges.reshape(-1), weights, ctypes.byref(st)))
+    else:
+        c = None if cores is None else np.ascontiguousarray(cores, np.float64)
+        _check(lib().oracle_boruvka_mrd(p, n, d, flags, int(k_pts), None if c is None else c.ctypes.data,
+                                        edges.reshape(-1), weights, ctypes.byref(st)))
     edges = edges[: n - 1]
     weights = weights[: n - 1]
     return OracleResult(

@@ -142,3 +142,28 @@ def test_oracle_large(large_golden, name):
     assert res.component_counts == rec["component_counts"]
     assert res.total_weight == rec["total_weight"]
     assert res.leaf_distance_evals == rec["leaf_distance_evals"]
+
+
+# ---------------------------------------------------------------- mutual reachability (§8f row 1)
+
+def test_oracle_core_distances_match_reference(mrd_golden):
+    """metric.py compute_core_distances, restated in oracle/emst_oracle.c, against the reference's values."""
+    arrays, meta = mrd_golden
+    for key in sorted(k for k in meta["cases"] if k != "given"):
+        name, k = key.rsplit("/", 1)
+        got = orc.core_distances(arrays[name + "/points"], int(k[1:]))
+        assert np.array_equal(got, arrays[key + "/core"]), key
+
+
+def test_oracle_mrd_mst_matches_reference(mrd_golden):
+    arrays, meta = mrd_golden
+    for key in sorted(k for k in meta["cases"] if k != "given"):
+        name, k = key.rsplit("/", 1)
+        rec = meta["cases"][key]
+        res = orc.boruvka_emst(arrays[name + "/points"], k_pts=int(k[1:]))
+        assert np.array_equal(res.edges, arrays[key + "/edges"]), key
+        assert np.array_equal(res.weights, arrays[key + "/weights"]), key
+        assert res.iterations == rec["iterations"] and res.component_counts == rec["component_counts"], key
+        assert res.total_weight == rec["total_weight"], key
+    res = orc.boruvka_emst(arrays["given/points"], cores=arrays["given/core"])
+    assert np.array_equal(res.edges, arrays["given/edges"]) and np.array_equal(res.weights, arrays["given/weights"])
