@@ -119,6 +119,14 @@ int emst_boruvka_mrd(emst_context* ctx, const float* pts, int64_t n, int32_t d, 
                      const double* core, int64_t* edges_out, double* weights_out, emst_stats* stats, char* err,
                      size_t errlen);
 
+/* Text formats of the reference's writers (data.py:117-141, 222-235), formatted on all host threads:
+ * emst_format_edges -> "u,v,%.17g\n" per edge; emst_format_points -> "%.9g" coordinates joined by ','
+ * and '\n' per row.  *out (length *len, not NUL-terminated) is owned by the library and valid until the
+ * next emst_format_* call or emst_text_free(); calls are not thread-safe. */
+int emst_format_edges(const int64_t* edges, const double* weights, int64_t m, const char** out, int64_t* len);
+int emst_format_points(const float* pts, int64_t n, int32_t d, const char** out, int64_t* len);
+void emst_text_free(void);
+
 /* compute_core_distances(build(points), points, k_pts) (metric.py:209-234): core_out n f64 (host), original
  * point order; k_pts in [1, n] (EMST_ERR_PARAM otherwise). */
 int emst_core_distances(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t k_pts,

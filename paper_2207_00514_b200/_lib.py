@@ -95,6 +95,9 @@ EXPORTS = (
     "emst_compute_upper_bounds",
     "emst_find_component_outgoing_edges",
     "emst_merge_components",
+    "emst_format_edges",
+    "emst_format_points",
+    "emst_text_free",
     "emst_build_info",
 )
 
@@ -139,9 +142,13 @@ def load():
         L.emst_compute_upper_bounds.argtypes = [vp, vp, i64, i32, vp, vp, vp, cp, sz]
         L.emst_find_component_outgoing_edges.argtypes = [vp, vp, i64, i32, vp, vp, vp, i32, vp, vp, vp, vp, cp, sz]
         L.emst_merge_components.argtypes = [vp, i64, vp, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, cp, sz]
-        L.emst_build_info.restype = ctypes.c_char_p
+        L.emst_format_edges.argtypes = [vp, vp, i64, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64)]
+        L.emst_format_points.argtypes = [vp, i64, i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64)]
+        L.emst_text_free.argtypes = []
         for name in EXPORTS:
-            getattr(L, name).restype = ctypes.c_int if name != "emst_build_info" else ctypes.c_char_p
+            getattr(L, name).restype = ctypes.c_int
+        L.emst_build_info.restype = ctypes.c_char_p
+        L.emst_text_free.restype = None
         _lib = L
         return L
 

@@ -19,6 +19,7 @@
 #include "core.cuh"
 #include "build.cuh"
 #include "radix_sort.cuh"
+#include "textio.h"
 #include "scan.cuh"
 
 using namespace emst;
@@ -754,6 +755,26 @@ void set_device(emst_context* c) { CK(cudaSetDevice(c->device)); }
 
 // ====================================================================== C ABI
 extern "C" {
+
+// ---- text I/O (textio.h): the reference's write_edges / write_points formats
+// Formats into a library-owned buffer; *out / *len stay valid until the next
+// call on any thread's behalf or emst_text_free().  (Host-only work.)
+static std::string g_text;
+int emst_format_edges(const int64_t* edges, const double* weights, int64_t m, const char** out, int64_t* len) {
+  if (m < 0 || (m > 0 && (!edges || !weights))) return EMST_ERR_PARAM;
+  g_text = emst_io::format_edges(edges, weights, m);
+  *out = g_text.data();
+  *len = (int64_t)g_text.size();
+  return EMST_OK;
+}
+int emst_format_points(const float* pts, int64_t n, int32_t d, const char** out, int64_t* len) {
+  if (n < 0 || (d != 2 && d != 3) || (n > 0 && !pts)) return EMST_ERR_PARAM;
+  g_text = emst_io::format_points(pts, n, d);
+  *out = g_text.data();
+  *len = (int64_t)g_text.size();
+  return EMST_OK;
+}
+void emst_text_free(void) { std::string().swap(g_text); }
 
 const char* emst_build_info(void) { return "emst_b200 sm_100a onesweep-lbvh-boruvka v1"; }
 

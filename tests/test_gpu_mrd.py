@@ -116,3 +116,15 @@ def test_mrd_building_blocks(mrd_golden):
     out = E.find_component_outgoing_edges(tree, pts, state, metric)
     # round 1 with singletons: each point's best edge is its mutual-reachability nearest neighbour
     assert np.isfinite(out.w[out.reps]).all() and out.w[out.reps].min() == arrays["normal3d_1000_s3/k4/weights"][0]
+
+
+def test_run_bench_reports():
+    """run_bench: the reference's report rows, on the GPU path."""
+    pts = E.generate(E.DatasetSpec("blobs", 20_000, 3, seed=0))
+    reps = E.run_bench(pts, [5_000, 20_000], repeats=2, dataset="blobs")
+    assert [r.n for r in reps] == [5_000, 20_000]
+    assert all(r.rate > 0 and r.t_total >= r.t_tree and r.iterations > 0 for r in reps)
+    assert np.isnan(reps[0].time_ratio_prev) and reps[1].time_ratio_prev > 0
+    assert reps[0].row().count("\t") == E.BenchReport.HEADER.count("\t")
+    mrd = E.run_bench(pts, [10_000], repeats=1, metric="mrd", k_pts=4)
+    assert mrd[0].t_core > 0

@@ -109,3 +109,9 @@ def test_oracle_is_not_imported_by_the_product():
     import pathlib
     for path in pathlib.Path(ROOT, "paper_2207_00514_b200").rglob("*.py"):
         assert "oracle" not in path.read_text().replace("Oracle", ""), path
+
+
+def test_run_bench_validates_before_any_gpu_work():
+    pts = E.generate(E.DatasetSpec("uniform", 100, 2, seed=0))
+    with pytest.raises(E.EmstError):
+        E.run_bench(pts, [10], repeats=0)
