@@ -191,7 +191,8 @@ __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __rest
   bool mixed = false;
   if (valid) {
     const int2 r = range[i];
-    const int2 refs = *reinterpret_cast<const int2*>(&nodes[i].ref.x);
+    const int4 ref4 = nodes[i].ref;   // child refs and the labels written last round
+    const int2 refs = make_int2(ref4.x, ref4.y);
     const int gamma = refs.x >= 0 ? refs.x : ~refs.x;
     const int bl = bprefix[r.x], bh = bprefix[r.y];
     mixed = bl != bh;
@@ -205,7 +206,9 @@ __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __rest
         if (refs.y >= 0 && lab.y != kMixed) { mark_lo[gamma + 1] = refs.y + 1; mark_hi[r.y] = refs.y + 1; }
       }
     }
-    *reinterpret_cast<int2*>(&nodes[i].ref.z) = lab;
+    // (a node that stays mixed with mixed children -- most of them early on --
+    // keeps its labels: no write, so its record's sector is not dirtied)
+    if (lab.x != ref4.z || lab.y != ref4.w) *reinterpret_cast<int2*>(&nodes[i].ref.z) = lab;
   }
   const unsigned keep = __ballot_sync(0xffffffffu, mixed);
   if (keep) {

@@ -113,8 +113,13 @@ __device__ __forceinline__ unsigned lanemask_lt_u32() {
 }
 
 constexpr int kTraverseThreads = 256;
-#ifndef EMST_TRAV_MINB
-#define EMST_TRAV_MINB 3
+// resident blocks per SM: 3D lanes use the extra registers (85) better, 2D
+// lanes prefer the extra warps (measured: 3D 3 blocks -1.5 %, 2D 4 blocks -17 %)
+#ifndef EMST_TRAV_MINB3
+#define EMST_TRAV_MINB3 3
+#endif
+#ifndef EMST_TRAV_MINB2
+#define EMST_TRAV_MINB2 4
 #endif
 #ifndef EMST_REFILL_IDLE
 #define EMST_REFILL_IDLE 16
@@ -251,7 +256,7 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
 // never conflict); deeper entries, rare, spill to a per-thread local array up to
 // the reference's capacity of 64 (bvh.py:36).
 template <int D, bool kSkip, bool kBounds, bool kMrd>
-__global__ void __launch_bounds__(kTraverseThreads, EMST_TRAV_MINB)
+__global__ void __launch_bounds__(kTraverseThreads, D == 3 ? EMST_TRAV_MINB3 : EMST_TRAV_MINB2)
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
