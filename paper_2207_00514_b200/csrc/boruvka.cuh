@@ -143,6 +143,56 @@ struct RoundScanOp {
   }
 };
 
+// Extra radius seeds for the solve (not the reference's building block): slot
+// s pairs with its Z-order neighbours s-W .. s+W (the direct neighbours are
+// already in the boundary scan).  A pair in different components is a real
+// outgoing edge, so its weight may lower s's component radius; only an upper
+// bound is needed, so it is f32 rounded up (+2^-40 slack) -- no
+// f64.  A block stages its slots +- W (labels, points) in shared memory once;
+// every slot takes the min over its 2W neighbours for its OWN component only
+// (each pair is seen from both sides) and sends one atomic if it can lower it.
+constexpr int kSeedThreads = 256;
+constexpr int kSeedMaxW = 32;
+
+template <int D>
+__global__ void __launch_bounds__(kSeedThreads) k_seed_window(const int* __restrict__ label,
+                                                              const float4* __restrict__ spts, long long n, int W,
+                                                              unsigned long long* ub) {
+  __shared__ float4 sp[kSeedThreads + 2 * kSeedMaxW];
+  __shared__ int sl[kSeedThreads + 2 * kSeedMaxW];
+  const long long base = blockIdx.x * (long long)kSeedThreads;
+  for (int i = threadIdx.x; i < kSeedThreads + 2 * W; i += kSeedThreads) {
+    const long long g = base - W + i;
+    const bool in = g >= 0 && g < n;
+    sl[i] = in ? label[g] : -1;
+    if (in) sp[i] = spts[g];
+  }
+  __syncthreads();
+  const long long s = base + threadIdx.x;
+  const int me = threadIdx.x + W;
+  const int ls = s < n ? sl[me] : -2;
+  const float4 pa = sp[me];
+  const float a[3] = {pa.x, pa.y, pa.z};
+  float best2 = __int_as_float(0x7f800000);
+  if (s < n) {
+    for (int k = 2; k <= W; ++k) {
+#pragma unroll
+      for (int dir = 0; dir < 2; ++dir) {
+        const int j = dir ? me + k : me - k;
+        const int lj = sl[j];
+        if (lj < 0 || lj == ls) continue;
+        const float4 pb = sp[j];
+        const float b[3] = {pb.x, pb.y, pb.z};
+        best2 = fminf(best2, point_ub2<D>(a, b));
+      }
+    }
+  }
+  unsigned long long w = best2 < __int_as_float(0x7f800000)
+                             ? (unsigned long long)__double_as_longlong(__dmul_ru((double)__fsqrt_ru(best2), 1.0 + 0x1p-40))
+                             : ~0ull;
+  if (ls >= 0 && w != ~0ull && w < __ldcg(&ub[ls])) atomicMin(&ub[ls], w);
+}
+
 // ------------------------------------------------------------- node labels
 // Also marks the "top pure" nodes: an internal child whose slot range lies in
 // one component while the node itself is mixed.  Every leaf under such a node T
