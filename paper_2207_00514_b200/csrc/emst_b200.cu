@@ -86,6 +86,7 @@ struct emst_context {
   int round = 0;                  // 1-based Boruvka round of the running solve (0 outside)
   int seed_window = 8;            // extra Z-order seed pairs (s +- 2..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
   long long round_comps = 0;      // components entering the running round
+  int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
@@ -401,7 +402,7 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds, c->core}, false);
   // window seeds pay while components are small and in 3D (measured: 37M blobs 3D
   // -2.3 ms, 10M normal 3D -0.6 ms; the 2D configs lose ~1 %); later rounds gain nothing
-  if (bounds && c->seed_window > 1 && c->dim == 3 && c->round >= 2 && !c->core && c->round_comps * 1024 >= n) {
+  if (bounds && c->seed_window > 1 && c->dim == 3 && c->round >= c->seed_from && !c->core && c->round_comps * 1024 >= n) {
     if (c->dim == 3) launch(c, k_seed_window<3>, grid_for(n, kSeedThreads), kSeedThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, std::min(c->seed_window, kSeedMaxW), c->ub.p);
     else launch(c, k_seed_window<2>, grid_for(n, kSeedThreads), kSeedThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, std::min(c->seed_window, kSeedMaxW), c->ub.p);
   }
@@ -807,6 +808,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     c = new emst_context();
     c->device = device;
     if (const char* t = getenv("EMST_SEED_WINDOW")) c->seed_window = atoi(t);
+    if (const char* t = getenv("EMST_SEED_FROM")) c->seed_from = atoi(t);
     c->rank = rank;
     c->world = world;
     set_device(c);
