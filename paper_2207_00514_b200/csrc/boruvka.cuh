@@ -194,14 +194,11 @@ __global__ void __launch_bounds__(kSeedThreads) k_seed_window(const int* __restr
 }
 
 // ------------------------------------------------------------- node labels
-// Also marks the "top pure" nodes: an internal child whose slot range lies in
-// one component while the node itself is mixed.  Every leaf under such a node T
-// has T as its highest single-component ancestor; the marks (T + 1 at the first
-// and the last slot of T's range) are turned into top[s] by k_scan<TopScan*>.
+// Reference semantics for every node (building blocks, subtree_skip off): a
+// child's label is uniform iff no boundary falls in its slot range.
 template <class Node>
 __global__ void k_node_labels(Node* __restrict__ nodes, const int2* __restrict__ range, const int* __restrict__ bprefix,
-                              const int* __restrict__ label, long long m, int* __restrict__ mark_lo,
-                              int* __restrict__ mark_hi) {
+                              const int* __restrict__ label, long long m) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= m) return;
   int2 r = range[i];
@@ -211,9 +208,31 @@ __global__ void k_node_labels(Node* __restrict__ nodes, const int2* __restrict__
   int ll = bg == bl ? label[r.x] : kMixed;
   int rl = bh == bg1 ? label[r.y] : kMixed;
   *reinterpret_cast<int2*>(&nodes[i].ref.z) = make_int2(ll, rl);
-  if (mark_lo && bl != bh) {
-    if (refs.x >= 0 && ll != kMixed) { mark_lo[r.x] = refs.x + 1; mark_hi[gamma] = refs.x + 1; }
-    if (refs.y >= 0 && rl != kMixed) { mark_lo[gamma + 1] = refs.y + 1; mark_hi[r.y] = refs.y + 1; }
+}
+
+constexpr int kDirectFill = 128;   // top pure nodes up to this many slots fill top[] themselves
+
+// top[s] = T + 1 for the top pure node T above slot s.  A top pure node (pure,
+// mixed parent) is re-marked every round by its parent, and the top pure node of
+// a slot only grows (pure stays pure), so filling the marked ranges each round
+// keeps top[] exact without clearing it (0 = the slot's parent is mixed).
+__device__ __forceinline__ void mark_top(int c, int lo, int hi, int* __restrict__ top, int* __restrict__ big,
+                                         unsigned* __restrict__ big_count) {
+  if (hi - lo + 1 <= kDirectFill) {
+    for (int s = lo; s <= hi; ++s) top[s] = c + 1;
+  } else {
+    big[atomicAdd(big_count, 1u)] = c;
+  }
+}
+
+// the larger marked ranges: one block per node (grid-stride over the list)
+__global__ void k_fill_top(const int2* __restrict__ range, const int* __restrict__ big,
+                           const unsigned* __restrict__ big_count, int* __restrict__ top) {
+  const unsigned cnt = *big_count;
+  for (unsigned i = blockIdx.x; i < cnt; i += gridDim.x) {
+    const int T = big[i];
+    const int2 r = range[T];
+    for (int s = r.x + (int)threadIdx.x; s <= r.y; s += blockDim.x) top[s] = T + 1;
   }
 }
 
@@ -233,8 +252,8 @@ template <class Node>
 __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __restrict__ range,
                                     const int* __restrict__ bprefix, const int* __restrict__ label,
                                     const int* __restrict__ list, long long count, int* __restrict__ out_list,
-                                    unsigned* __restrict__ out_count, int* __restrict__ mark_lo,
-                                    int* __restrict__ mark_hi) {
+                                    unsigned* __restrict__ out_count, int* __restrict__ top, int* __restrict__ big,
+                                    unsigned* __restrict__ big_count) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool valid = t < count;
   const int i = valid ? (list ? list[t] : (int)t) : 0;
@@ -251,9 +270,9 @@ __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __rest
       const int bg = bprefix[gamma], bg1 = bprefix[gamma + 1];
       lab.x = bg == bl ? label[r.x] : kMixed;
       lab.y = bh == bg1 ? label[r.y] : kMixed;
-      if (mark_lo) {
-        if (refs.x >= 0 && lab.x != kMixed) { mark_lo[r.x] = refs.x + 1; mark_hi[gamma] = refs.x + 1; }
-        if (refs.y >= 0 && lab.y != kMixed) { mark_lo[gamma + 1] = refs.y + 1; mark_hi[r.y] = refs.y + 1; }
+      if (top) {
+        if (refs.x >= 0 && lab.x != kMixed) mark_top(refs.x, r.x, gamma, top, big, big_count);
+        if (refs.y >= 0 && lab.y != kMixed) mark_top(refs.y, gamma + 1, r.y, top, big, big_count);
       }
     }
     // (a node that stays mixed with mixed children -- most of them early on --
@@ -269,45 +288,6 @@ __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __rest
     if (mixed) out_list[base + __popc(keep & ((1u << lane) - 1u))] = i;
   }
 }
-
-// top[s] = T + 1 for the top pure node T whose range holds slot s, else 0.  The
-// ranges are disjoint, so top[s] = sum_{j <= s} mark_lo[j] - sum_{j < s} mark_hi[j]:
-// an exclusive scan of (mark_lo - mark_hi) plus mark_lo[s], in wrapping u32
-// arithmetic (exact, every true prefix is in [0, 2^30)).  The store clears the
-// marks for the next round (each index is read and cleared by one thread).
-struct TopScanOp {
-  using T = unsigned;
-  __device__ void side(long long, int, const unsigned*) const {}
-  int* mark_lo;
-  int* mark_hi;
-  int* top;
-  __device__ void load(long long i0, int cnt, unsigned* v) const {
-    int lo[kScanItems], hi[kScanItems];
-    load8(mark_lo, i0, cnt, lo);
-    load8(mark_hi, i0, cnt, hi);
-#pragma unroll
-    for (int j = 0; j < kScanItems; ++j) v[j] = j < cnt ? (unsigned)lo[j] - (unsigned)hi[j] : 0u;
-  }
-  __device__ void store(long long i0, int cnt, const unsigned* v, unsigned ex) const {
-    int out[kScanItems];
-    unsigned nz = 0;
-#pragma unroll
-    for (int j = 0; j < kScanItems; ++j) {
-      // v[j] = lo - hi; the start mark lo is 0 unless a range opens here, and a
-      // range of >= 2 slots never opens and closes on the same slot
-      const int lo = j < cnt ? __ldg(mark_lo + i0 + j) : 0;
-      out[j] = (int)(ex + (unsigned)lo);
-      ex += v[j];
-      nz |= v[j];
-    }
-    store8(top, i0, cnt, out);
-    if (nz) {
-#pragma unroll
-      for (int j = 0; j < kScanItems; ++j)
-        if (j < cnt && v[j]) { mark_lo[i0 + j] = 0; mark_hi[i0 + j] = 0; }
-    }
-  }
-};
 
 // ------------------------------------------------------------------- merge
 constexpr int kErrNoEdge = 1;     // mst.py:365-376 / 720-721

@@ -78,7 +78,7 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 }  // namespace
 
 constexpr int kCounters = 16;   // [0] evals [1] scan total [2] err [3] overflow [4] work [5] visits
-                                // [6] found [7] ties [8] frontier size [9] skipped queries
+                                // [6] found [7] ties [8] frontier size [9] skipped queries [10] big tops
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
@@ -115,7 +115,7 @@ struct emst_context {
   // rounds
   DevBuf<int> label, bprefix;
   DevBuf<float> nfn_lb;   // per slot: proven lower bound on the nearest-foreign distance
-  DevBuf<int> mark_lo, mark_hi, top;   // top pure node per slot (T + 1, 0 = none)
+  DevBuf<int> top, big_tops;           // top pure node per slot (T + 1, 0 = none); large ones to fill
   DevBuf<int> front[2];                // internal nodes still mixed after the last labelling
   // mutual reachability: core distance per slot; `core` points at it while a
   // mutual-reachability solve / building block runs, nullptr for Euclidean
@@ -338,10 +338,9 @@ void ensure_rounds(emst_context* c, long long n) {
   c->label.ensure(n);
   c->bprefix.ensure(n);
   c->nfn_lb.ensure(n);
-  c->mark_lo.ensure(n);
+  c->big_tops.ensure(n / kDirectFill + 1);
   c->front[0].ensure(std::max<long long>(n - 1, 1));
   c->front[1].ensure(std::max<long long>(n - 1, 1));
-  c->mark_hi.ensure(n);
   c->top.ensure(n);
   c->ub.ensure(n);
   c->best.ensure(n);
@@ -375,14 +374,14 @@ enum LabelMode {
 template <class Node>
 void launch_labels(emst_context* c, long long n, LabelMode mode, bool want_top) {
   const long long m = n - 1;
-  int* mlo = want_top ? c->mark_lo.p : nullptr;
-  int* mhi = want_top ? c->mark_hi.p : nullptr;
   Node* nodes = reinterpret_cast<Node*>(c->nodes.p);
   if (mode == kLabelsFull) {
     launch(c, k_node_labels<Node>, grid_for(m, 256), 256, 0, nodes, (const int2*)c->range.p, (const int*)c->bprefix.p,
-           (const int*)c->label.p, m, mlo, mhi);
+           (const int*)c->label.p, m);
     return;
   }
+  unsigned* big_n = reinterpret_cast<unsigned*>(dev_counter(c, 10));
+  CK(cudaMemsetAsync(big_n, 0, sizeof(long long), c->stream));
   const long long count = c->front_n < 0 ? m : c->front_n;
   const int* in = c->front_n < 0 ? nullptr : c->front[c->front_cur].p;
   int* out = c->front[c->front_cur ^ 1].p;
@@ -390,7 +389,11 @@ void launch_labels(emst_context* c, long long n, LabelMode mode, bool want_top) 
   CK(cudaMemsetAsync(out_n, 0, sizeof(long long), c->stream));
   if (count > 0)
     launch(c, k_node_labels_front<Node>, grid_for(count, 256), 256, 0, nodes, (const int2*)c->range.p,
-           (const int*)c->bprefix.p, (const int*)c->label.p, in, count, out, out_n, mlo, mhi);
+           (const int*)c->bprefix.p, (const int*)c->label.p, in, count, out, out_n,
+           want_top ? c->top.p : (int*)nullptr, c->big_tops.p, big_n);
+  if (want_top)
+    launch(c, k_fill_top, (unsigned)c->num_sms * 4, 256, 0, (const int2*)c->range.p, (const int*)c->big_tops.p,
+           (const unsigned*)big_n, c->top.p);
   c->front_cur ^= 1;
   c->front_pending = true;   // front_n is read back with the round's counters
 }
@@ -410,10 +413,7 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   if (n > 1 && mode != kLabelsNone) {
     if (c->dim == 3) launch_labels<Node3>(c, n, mode, want_top);
     else launch_labels<Node2>(c, n, mode, want_top);
-    if (want_top) {
-      run_scan(c, n, TopScanOp{c->mark_lo.p, c->mark_hi.p, c->top.p}, false);
-      c->top_valid = true;
-    }
+    c->top_valid = want_top && mode == kLabelsFrontier;
   }
   cudaEvent_t ev_c;
   CK(cudaEventCreate(&ev_c));
@@ -666,9 +666,8 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
   launch(c, k_iota_int, grid_for(n, 256), 256, 0, c->label.p, n);
   CK(cudaMemsetAsync(c->nfn_lb.p, 0, n * sizeof(float), c->stream));
-  CK(cudaMemsetAsync(c->mark_lo.p, 0, n * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(c->top.p, 0, n * sizeof(int), c->stream));
   c->front_n = -1;
-  CK(cudaMemsetAsync(c->mark_hi.p, 0, n * sizeof(int), c->stream));
   long long comps = n, edges = 0;
   const int max_it = max_iterations(n);
   st->component_counts[0] = n;
@@ -845,7 +844,7 @@ int emst_context_destroy(emst_context* c) {
   c->sort_hist.release(); c->sort_off.release(); c->sort_status.release(); c->sort_misc.release();
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
   c->node_parent.release(); c->leaf_parent.release(); c->node_delta.release(); c->up.release(); c->arrivals.release(); c->root_box.release();
-  c->label.release(); c->bprefix.release(); c->mark_lo.release(); c->mark_hi.release(); c->top.release();
+  c->label.release(); c->bprefix.release(); c->big_tops.release(); c->top.release();
   c->front[0].release(); c->front[1].release(); c->core_slot.release(); c->core_tmp.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
