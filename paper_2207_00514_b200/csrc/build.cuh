@@ -206,16 +206,74 @@ __device__ __forceinline__ void get_union_box(const Node2* nodes, int node, floa
   lo[2] = hi[2] = 0.f;
 }
 
+// both child boxes of a node at once (sides a = left, b = right), vector stores
+__device__ __forceinline__ void put_node_boxes(Node3* nodes, int node, const float* alo, const float* ahi,
+                                               const float* blo, const float* bhi) {
+  float4* p = reinterpret_cast<float4*>(&nodes[node]);
+  p[0] = make_float4(alo[0], blo[0], alo[1], blo[1]);
+  p[1] = make_float4(alo[2], blo[2], ahi[0], bhi[0]);
+  p[2] = make_float4(ahi[1], bhi[1], ahi[2], bhi[2]);
+}
+__device__ __forceinline__ void put_node_boxes(Node2* nodes, int node, const float* alo, const float* ahi,
+                                               const float* blo, const float* bhi) {
+  float4* p = reinterpret_cast<float4*>(&nodes[node]);
+  p[0] = make_float4(alo[0], blo[0], alo[1], blo[1]);
+  p[1] = make_float4(ahi[0], bhi[0], ahi[1], bhi[1]);
+}
+
+constexpr int kRefitThreads = 256;
+
+// Bottom-up boxes, one thread per leaf, in two phases.  A block owns the
+// kRefitThreads consecutive slots [B, B+T); a node whose slot range lies inside
+// it (Karras: then its index is in [B, B+T) too) has all its leaves in this
+// block, so its arrivals are counted in shared memory and the first arrival
+// parks its box there: no global atomics or fences, and the second arrival
+// writes the node's two child boxes with three 16-byte stores.  The first node
+// that straddles the block edge, and every ancestor of it, uses the global
+// protocol: child box into the record, acq_rel arrival count, the second
+// arrival reads both boxes back from L2.
 template <class Node>
-__global__ void k_refit(const float4* __restrict__ spts, long long n, Node* nodes, const int* __restrict__ node_parent,
-                        const int* __restrict__ leaf_parent, unsigned* __restrict__ arrivals, Box3* __restrict__ root_box) {
-  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void __launch_bounds__(kRefitThreads)
+k_refit(const float4* __restrict__ spts, long long n, Node* nodes, const int2* __restrict__ range,
+        const int* __restrict__ node_parent, const int* __restrict__ leaf_parent, unsigned* __restrict__ arrivals,
+        Box3* __restrict__ root_box) {
+  __shared__ unsigned s_arr[kRefitThreads];
+  __shared__ float s_box[kRefitThreads][2][6];
+  const long long B = (long long)blockIdx.x * kRefitThreads;
+  s_arr[threadIdx.x] = 0;
+  __syncthreads();
+  const long long s = B + threadIdx.x;
   if (s >= n) return;
-  float4 p = spts[s];
+  const long long E = min(B + kRefitThreads, n);   // block's slots: [B, E)
+  const float4 p = spts[s];
   float lo[3] = {p.x, p.y, p.z}, hi[3] = {p.x, p.y, p.z};
   int link = leaf_parent[s];
   for (;;) {
-    int node = link >> 1, side = link & 1;
+    const int node = link >> 1, side = link & 1;
+    const int2 r = range[node];
+    if (r.x < B || r.y >= E) break;
+    float* mine = s_box[node - B][side];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { mine[k] = lo[k]; mine[3 + k] = hi[k]; }
+    __threadfence_block();
+    if (atomicAdd(&s_arr[node - B], 1u) == 0) return;
+    __threadfence_block();
+    const float* other = s_box[node - B][side ^ 1];
+    float olo[3], ohi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { olo[k] = other[k]; ohi[k] = other[3 + k]; }
+    if (side == 0) put_node_boxes(nodes, node, lo, hi, olo, ohi);
+    else put_node_boxes(nodes, node, olo, ohi, lo, hi);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { lo[k] = fminf(lo[k], olo[k]); hi[k] = fmaxf(hi[k], ohi[k]); }
+    if (node == 0) {
+      for (int k = 0; k < 3; ++k) { root_box->lo[k] = lo[k]; root_box->hi[k] = hi[k]; }
+      return;
+    }
+    link = node_parent[node];
+  }
+  for (;;) {
+    const int node = link >> 1, side = link & 1;
     put_child_box(nodes, node, side, lo, hi);
     // acq_rel: the first arrival's box is released by its increment and the
     // second arrival acquires it with its own (no full fences needed)

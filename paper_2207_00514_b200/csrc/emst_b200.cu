@@ -303,13 +303,15 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
       Node3* nodes = reinterpret_cast<Node3*>(c->nodes.p);
       launch(c, k_karras<Node3>, grid_for(m, 256), 256, 0, (const unsigned long long*)skeys, n, nodes, c->range.p,
              c->node_parent.p, c->leaf_parent.p, c->node_delta.p);
-      launch(c, k_refit<Node3>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, nodes,
+      launch(c, k_refit<Node3>, grid_for(n, kRefitThreads), kRefitThreads, 0, (const float4*)c->spts.p, n, nodes,
+             (const int2*)c->range.p,
              (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p);
     } else {
       Node2* nodes = reinterpret_cast<Node2*>(c->nodes.p);
       launch(c, k_karras<Node2>, grid_for(m, 256), 256, 0, (const unsigned long long*)skeys, n, nodes, c->range.p,
              c->node_parent.p, c->leaf_parent.p, c->node_delta.p);
-      launch(c, k_refit<Node2>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, nodes,
+      launch(c, k_refit<Node2>, grid_for(n, kRefitThreads), kRefitThreads, 0, (const float4*)c->spts.p, n, nodes,
+             (const int2*)c->range.p,
              (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p);
     }
   }
