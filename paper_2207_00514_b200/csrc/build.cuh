@@ -114,19 +114,43 @@ __global__ void k_morton(const float* __restrict__ pts, long long n, const Scene
   }
 }
 
+// Slot-order points: kGatherPer slots per thread so that many independent
+// random point reads are in flight per thread (the reads follow the Morton
+// permutation and are latency-bound); also writes perm and its inverse.
+constexpr int kGatherThreads = 256;
+constexpr int kGatherPer = 4;
+
 template <int D>
-__global__ void k_gather(const float* __restrict__ pts, long long n, const unsigned* __restrict__ perm,
-                         float4* __restrict__ spts, unsigned* __restrict__ iperm) {
-  long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  unsigned p = perm[s];
-  float4 v;
-  v.x = pts[(long long)p * D + 0];
-  v.y = pts[(long long)p * D + 1];
-  v.z = D == 3 ? pts[(long long)p * D + 2] : 0.f;
-  v.w = __uint_as_float(p);
-  spts[s] = v;
-  iperm[p] = (unsigned)s;
+__global__ void __launch_bounds__(kGatherThreads)
+k_gather(const float* __restrict__ pts, long long n, const unsigned* __restrict__ sorted_idx,
+         unsigned* __restrict__ perm, float4* __restrict__ spts, unsigned* __restrict__ iperm) {
+  const long long base = (long long)blockIdx.x * (kGatherThreads * kGatherPer) + threadIdx.x;
+  unsigned p[kGatherPer];
+  float4 v[kGatherPer];
+#pragma unroll
+  for (int j = 0; j < kGatherPer; ++j) {
+    const long long s = base + j * kGatherThreads;
+    p[j] = s < n ? sorted_idx[s] : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < kGatherPer; ++j) {
+    const long long s = base + j * kGatherThreads;
+    if (s < n) {
+      v[j].x = pts[(long long)p[j] * D + 0];
+      v[j].y = pts[(long long)p[j] * D + 1];
+      v[j].z = D == 3 ? pts[(long long)p[j] * D + 2] : 0.f;
+      v[j].w = __uint_as_float(p[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kGatherPer; ++j) {
+    const long long s = base + j * kGatherThreads;
+    if (s < n) {
+      spts[s] = v[j];
+      perm[s] = p[j];
+      iperm[p[j]] = (unsigned)s;
+    }
+  }
 }
 
 // Common-prefix length of augmented keys (code, slot); -1 out of range (bvh.py:138-149).
@@ -221,7 +245,10 @@ __device__ __forceinline__ void put_node_boxes(Node2* nodes, int node, const flo
   p[1] = make_float4(ahi[0], bhi[0], ahi[1], bhi[1]);
 }
 
-constexpr int kRefitThreads = 256;
+#ifndef EMST_REFIT_THREADS
+#define EMST_REFIT_THREADS 256
+#endif
+constexpr int kRefitThreads = EMST_REFIT_THREADS;
 
 // Bottom-up boxes, one thread per leaf, in two phases.  A block owns the
 // kRefitThreads consecutive slots [B, B+T); a node whose slot range lies inside

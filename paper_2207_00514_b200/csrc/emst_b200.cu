@@ -293,9 +293,11 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
   unsigned* svals;
   radix_sort(c, n, d == 3 ? 63 : 62, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &skeys, &svals);
   // sorted codes -> k-buffer `skeys`, permutation -> `svals`
-  CK(cudaMemcpyAsync(c->perm.p, svals, n * sizeof(unsigned), cudaMemcpyDeviceToDevice, c->stream));
-  if (d == 3) launch(c, k_gather<3>, grid_for(n, 256), 256, 0, dev_pts, n, (const unsigned*)c->perm.p, c->spts.p, c->iperm.p);
-  else launch(c, k_gather<2>, grid_for(n, 256), 256, 0, dev_pts, n, (const unsigned*)c->perm.p, c->spts.p, c->iperm.p);
+  {
+    const unsigned g = grid_for(n, kGatherThreads * kGatherPer);
+    if (d == 3) launch(c, k_gather<3>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, c->iperm.p);
+    else launch(c, k_gather<2>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, c->iperm.p);
+  }
   if (n > 1) {
     const long long m = n - 1;
     CK(cudaMemsetAsync(c->arrivals.p, 0, m * sizeof(unsigned), c->stream));
