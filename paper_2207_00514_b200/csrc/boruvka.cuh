@@ -216,23 +216,31 @@ constexpr int kDirectFill = 128;   // top pure nodes up to this many slots fill 
 // mixed parent) is re-marked every round by its parent, and the top pure node of
 // a slot only grows (pure stays pure), so filling the marked ranges each round
 // keeps top[] exact without clearing it (0 = the slot's parent is mixed).
-__device__ __forceinline__ void mark_top(int c, int lo, int hi, int* __restrict__ top, int* __restrict__ big,
+constexpr int kFillChunk = 1024;   // larger ones are cut into chunks of this many slots, a warp each
+
+__device__ __forceinline__ void mark_top(int c, int lo, int hi, int* __restrict__ top, int4* __restrict__ big,
                                          unsigned* __restrict__ big_count) {
   if (hi - lo + 1 <= kDirectFill) {
     for (int s = lo; s <= hi; ++s) top[s] = c + 1;
   } else {
-    big[atomicAdd(big_count, 1u)] = c;
+    const int k = (hi - lo + kFillChunk) / kFillChunk;
+    const unsigned base = atomicAdd(big_count, (unsigned)k);
+    for (int j = 0; j < k; ++j) {
+      const int a = lo + j * kFillChunk;
+      big[base + j] = make_int4(c + 1, a, min(hi, a + kFillChunk - 1), 0);
+    }
   }
 }
 
-// the larger marked ranges: one block per node (grid-stride over the list)
-__global__ void k_fill_top(const int2* __restrict__ range, const int* __restrict__ big,
-                           const unsigned* __restrict__ big_count, int* __restrict__ top) {
+// the chunks of the larger ranges (disjoint: top pure nodes never nest), a warp per chunk
+__global__ void k_fill_top(const int4* __restrict__ big, const unsigned* __restrict__ big_count,
+                           int* __restrict__ top) {
   const unsigned cnt = *big_count;
-  for (unsigned i = blockIdx.x; i < cnt; i += gridDim.x) {
-    const int T = big[i];
-    const int2 r = range[T];
-    for (int s = r.x + (int)threadIdx.x; s <= r.y; s += blockDim.x) top[s] = T + 1;
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned warps = gridDim.x * (blockDim.x >> 5);
+  for (unsigned w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < cnt; w += warps) {
+    const int4 it = big[w];
+    for (int s = it.y + (int)lane; s <= it.z; s += 32) top[s] = it.x;
   }
 }
 
@@ -252,7 +260,7 @@ template <class Node>
 __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __restrict__ range,
                                     const int* __restrict__ bprefix, const int* __restrict__ label,
                                     const int* __restrict__ list, long long count, int* __restrict__ out_list,
-                                    unsigned* __restrict__ out_count, int* __restrict__ top, int* __restrict__ big,
+                                    unsigned* __restrict__ out_count, int* __restrict__ top, int4* __restrict__ big,
                                     unsigned* __restrict__ big_count) {
   const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool valid = t < count;

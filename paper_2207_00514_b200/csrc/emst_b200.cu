@@ -115,7 +115,8 @@ struct emst_context {
   // rounds
   DevBuf<int> label, bprefix;
   DevBuf<float> nfn_lb;   // per slot: proven lower bound on the nearest-foreign distance
-  DevBuf<int> top, big_tops;           // top pure node per slot (T + 1, 0 = none); large ones to fill
+  DevBuf<int> top;
+  DevBuf<int4> big_tops;           // top pure node per slot (T + 1, 0 = none); large ones to fill
   DevBuf<int> front[2];                // internal nodes still mixed after the last labelling
   // mutual reachability: core distance per slot; `core` points at it while a
   // mutual-reachability solve / building block runs, nullptr for Euclidean
@@ -342,7 +343,7 @@ void ensure_rounds(emst_context* c, long long n) {
   c->label.ensure(n);
   c->bprefix.ensure(n);
   c->nfn_lb.ensure(n);
-  c->big_tops.ensure(n / kDirectFill + 1);
+  c->big_tops.ensure(n / kDirectFill + n / kFillChunk + 2);   // top pure ranges are disjoint
   c->front[0].ensure(std::max<long long>(n - 1, 1));
   c->front[1].ensure(std::max<long long>(n - 1, 1));
   c->top.ensure(n);
@@ -396,7 +397,7 @@ void launch_labels(emst_context* c, long long n, LabelMode mode, bool want_top) 
            (const int*)c->bprefix.p, (const int*)c->label.p, in, count, out, out_n,
            want_top ? c->top.p : (int*)nullptr, c->big_tops.p, big_n);
   if (want_top)
-    launch(c, k_fill_top, (unsigned)c->num_sms * 4, 256, 0, (const int2*)c->range.p, (const int*)c->big_tops.p,
+    launch(c, k_fill_top, (unsigned)c->num_sms * 8, 256, 0, (const int4*)c->big_tops.p,
            (const unsigned*)big_n, c->top.p);
   c->front_cur ^= 1;
   c->front_pending = true;   // front_n is read back with the round's counters
