@@ -146,47 +146,69 @@ struct RoundScanOp {
 // Extra radius seeds for the solve (not the reference's building block): slot
 // s pairs with its Z-order neighbours s-W .. s+W (the direct neighbours are
 // already in the boundary scan).  A pair in different components is a real
-// outgoing edge, so its weight may lower s's component radius; only an upper
+// outgoing edge, so its weight may lower both components' radii; only an upper
 // bound is needed, so it is f32 rounded up (+2^-40 slack) -- no
-// f64.  A block stages its slots +- W (labels, points) in shared memory once;
-// every slot takes the min over its 2W neighbours for its OWN component only
-// (each pair is seen from both sides) and sends one atomic if it can lower it.
+// f64.  A block stages its slots [base, base+T) and W on either side (labels,
+// points) in shared memory once.  Each pair (i, i+k), k = 2..W, is computed
+// once, by the thread of its lower slot (including the W slots left of the
+// block): the lower end keeps a register minimum, the upper end gets a
+// shared-memory atomic min (squared f32 bounds >= 0 order as their bits).
+// Every slot then sends one global atomic if it can lower its component's bound.
 constexpr int kSeedThreads = 256;
 constexpr int kSeedMaxW = 32;
 
-template <int D>
+template <int D, int kW>
+__device__ __forceinline__ float seed_pairs(const float4* sp, const int* sl, unsigned* s_best, int a, int lim, int W) {
+  const int la = sl[a];
+  float mine = __int_as_float(0x7f800000);
+  if (la < 0) return mine;
+  const float4 pa = sp[a];
+  const float q[3] = {pa.x, pa.y, pa.z};
+  const int kmax = kW ? kW : W;
+#pragma unroll
+  for (int k = 2; k <= (kW ? kW : kSeedMaxW); ++k) {
+    if (!kW && k > kmax) break;
+    const int b = a + k;
+    if (b >= lim) break;
+    const int lb = sl[b];
+    if (lb < 0 || lb == la) continue;
+    const float4 pb = sp[b];
+    const float p[3] = {pb.x, pb.y, pb.z};
+    const float d2 = point_ub2<D>(q, p);
+    mine = fminf(mine, d2);
+    if (b >= W + 0 && b - W < kSeedThreads) atomicMin(&s_best[b - W], __float_as_uint(d2));
+  }
+  return mine;
+}
+
+template <int D, int kW>
 __global__ void __launch_bounds__(kSeedThreads) k_seed_window(const int* __restrict__ label,
                                                               const float4* __restrict__ spts, long long n, int W,
                                                               unsigned long long* ub) {
   __shared__ float4 sp[kSeedThreads + 2 * kSeedMaxW];
   __shared__ int sl[kSeedThreads + 2 * kSeedMaxW];
+  __shared__ unsigned s_best[kSeedThreads];
+  if (kW) W = kW;
   const long long base = blockIdx.x * (long long)kSeedThreads;
-  for (int i = threadIdx.x; i < kSeedThreads + 2 * W; i += kSeedThreads) {
+  const int lim = kSeedThreads + 2 * W;
+  for (int i = threadIdx.x; i < lim; i += kSeedThreads) {
     const long long g = base - W + i;
     const bool in = g >= 0 && g < n;
     sl[i] = in ? label[g] : -1;
     if (in) sp[i] = spts[g];
   }
+  s_best[threadIdx.x] = 0x7f800000u;
   __syncthreads();
-  const long long s = base + threadIdx.x;
+  // sources: staged slots [0, T + W) -- the left halo and the block itself
   const int me = threadIdx.x + W;
-  const int ls = s < n ? sl[me] : -2;
-  const float4 pa = sp[me];
-  const float a[3] = {pa.x, pa.y, pa.z};
-  float best2 = __int_as_float(0x7f800000);
-  if (s < n) {
-    for (int k = 2; k <= W; ++k) {
-#pragma unroll
-      for (int dir = 0; dir < 2; ++dir) {
-        const int j = dir ? me + k : me - k;
-        const int lj = sl[j];
-        if (lj < 0 || lj == ls) continue;
-        const float4 pb = sp[j];
-        const float b[3] = {pb.x, pb.y, pb.z};
-        best2 = fminf(best2, point_ub2<D>(a, b));
-      }
-    }
+  float best2 = seed_pairs<D, kW>(sp, sl, s_best, me, lim, W);
+  if (threadIdx.x < W) {
+    const float h = seed_pairs<D, kW>(sp, sl, s_best, threadIdx.x, lim, W);   // halo source: upper ends only
+    (void)h;
   }
+  __syncthreads();
+  best2 = fminf(best2, __uint_as_float(s_best[threadIdx.x]));
+  const int ls = sl[me];
   unsigned long long w = best2 < __int_as_float(0x7f800000)
                              ? (unsigned long long)__double_as_longlong(__dmul_ru((double)__fsqrt_ru(best2), 1.0 + 0x1p-40))
                              : ~0ull;

@@ -411,8 +411,11 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   // window seeds pay while components are small and in 3D (measured: 37M blobs 3D
   // -2.3 ms, 10M normal 3D -0.6 ms; the 2D configs lose ~1 %); later rounds gain nothing
   if (bounds && c->seed_window > 1 && c->dim == 3 && c->round >= c->seed_from && !c->core && c->round_comps * 1024 >= n) {
-    if (c->dim == 3) launch(c, k_seed_window<3>, grid_for(n, kSeedThreads), kSeedThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, std::min(c->seed_window, kSeedMaxW), c->ub.p);
-    else launch(c, k_seed_window<2>, grid_for(n, kSeedThreads), kSeedThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, std::min(c->seed_window, kSeedMaxW), c->ub.p);
+    const int W = std::min(c->seed_window, kSeedMaxW);
+    const auto kern = c->dim == 3 ? (W == 8 ? k_seed_window<3, 8> : k_seed_window<3, 0>)
+                                  : (W == 8 ? k_seed_window<2, 8> : k_seed_window<2, 0>);
+    launch(c, kern, grid_for(n, kSeedThreads), kSeedThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, W,
+           c->ub.p);
   }
   CK(cudaEventRecord(c->ev_b, c->stream));
   if (n > 1 && mode != kLabelsNone) {
