@@ -191,3 +191,23 @@ def test_full_size_configs(large_golden, name):
     assert e.shape == (s["n"] - 1, 2) and np.all(e[:, 0] < e[:, 1])
     w = res.weights
     assert np.all(np.diff(w) >= 0)
+
+
+@pytest.mark.parametrize("case", ["identical_3d", "lattice_3d", "lattice_2d_dups"])
+def test_massive_ties_match_oracle(case):
+    """Tie runs longer than one block (> 4096 equal weights) take the two-key edge order; the
+    oracle restatement (pinned to the reference by test_oracle_golden) is the checker."""
+    from oracle import oracle as orc
+    if case == "identical_3d":
+        pts = np.full((10000, 3), 0.25, np.float32)
+    elif case == "lattice_3d":
+        g = np.arange(24, dtype=np.float32) / 8
+        pts = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    else:
+        g = np.arange(100, dtype=np.float32)
+        pts = np.stack(np.meshgrid(g, g, indexing="ij"), -1).reshape(-1, 2)
+        pts = np.concatenate([pts, pts[::3]])
+    res = E.boruvka_emst(pts)
+    ref = orc.boruvka_emst(pts)
+    assert np.array_equal(res.edges, ref.edges) and np.array_equal(res.weights, ref.weights), case
+    assert res.iterations == ref.iterations and list(res.component_counts) == list(ref.component_counts)
