@@ -466,46 +466,110 @@ __global__ void k_virtual_reduce(const EdgeKey* __restrict__ shard_keys, int sha
 }
 
 // ------------------------------------------------------------ final output
-constexpr int kShortTie = 32;     // tie runs up to this long are ordered in place by one thread
+constexpr int kThreadTie = 8;     // tie runs up to this long are ordered in registers by one thread
+constexpr int kShortTie = 32;     // ... up to this long by one warp each
 constexpr int kBlockTie = 4096;   // longer ones up to this long by one block each
 
-// Scan the weight-sorted edges for runs of equal weights: the longest run
-// (capped at kBlockTie + 1) goes to *max_run, and every run longer than
-// kShortTie but at most kBlockTie is appended to `runs` as (start, length).
-__global__ void k_edge_ties(const unsigned long long* __restrict__ w, long long ne, unsigned* __restrict__ max_run,
-                            int2* __restrict__ runs, unsigned* __restrict__ run_count) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i + 1 >= ne || w[i] != w[i + 1] || (i > 0 && w[i - 1] == w[i])) return;   // run starts only
-  unsigned len = 2;
-  while (len <= (unsigned)kBlockTie && i + len < ne && w[i + len] == w[i]) ++len;
-  atomicMax(max_run, len);
-  if (len > (unsigned)kShortTie && len <= (unsigned)kBlockTie) runs[atomicAdd(run_count, 1u)] = make_int2((int)i, (int)len);
+// One pass over the weight-sorted edges.  The thread at the start of each run
+// of equal weights measures it and puts it into (u, v) order (the uv keys are
+// distinct): a run of at most kThreadTie edges itself, in registers; a longer
+// one of at most kShortTie is listed in `mid` for a warp (k_edge_fix_mid), one
+// of at most kBlockTie in `runs` for a block (k_edge_fix_long), as (start,
+// length); a still longer run raises *max_run above kBlockTie and the host
+// switches to the two-key sort.
+__global__ void k_edge_ties(const unsigned long long* __restrict__ w, long long ne,
+                            const unsigned long long* __restrict__ euv, unsigned* __restrict__ order,
+                            unsigned* __restrict__ max_run, int2* __restrict__ runs, unsigned* __restrict__ run_count,
+                            int2* __restrict__ mid, unsigned* __restrict__ mid_count) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  int len = 0;
+  if (i + 1 < ne) {
+    const unsigned long long wi = w[i];
+    if (wi == w[i + 1] && (i == 0 || w[i - 1] != wi)) {   // a run starts here
+      // run length by galloping + binary search (the keys are sorted), capped at kBlockTie + 1
+      const long long cap = min(ne, i + kBlockTie + 1);   // positions [i, cap) may belong to the run
+      long long lo = i + 1, hi = i + 2;                   // w[lo] == wi; hi: first candidate to test
+      while (hi < cap && w[hi] == wi) {
+        lo = hi;
+        hi = min(cap, i + 2 * (hi - i));
+      }
+      while (hi - lo > 1) {   // last equal position in [lo, hi)
+        const long long m = (lo + hi) >> 1;
+        if (w[m] == wi) lo = m; else hi = m;
+      }
+      len = (int)(lo - i + 1);
+    }
+  }
+  if (len == 2) {
+    const unsigned o0 = order[i], o1 = order[i + 1];
+    if (euv[o0] > euv[o1]) { order[i] = o1; order[i + 1] = o0; }
+  } else if (len > 2 && len <= kThreadTie) {
+    // in registers: all loads issued at once, then a fixed compare-exchange network
+    unsigned o[kThreadTie];
+    unsigned long long k[kThreadTie];
+#pragma unroll
+    for (int a = 0; a < kThreadTie; ++a) o[a] = a < len ? order[i + a] : 0u;
+#pragma unroll
+    for (int a = 0; a < kThreadTie; ++a) k[a] = a < len ? euv[o[a]] : ~0ull;
+#pragma unroll
+    for (int a = 1; a < kThreadTie; ++a) {
+#pragma unroll
+      for (int b = a; b > 0; --b) {
+        if (k[b - 1] > k[b]) {
+          const unsigned long long t = k[b - 1]; k[b - 1] = k[b]; k[b] = t;
+          const unsigned u = o[b - 1]; o[b - 1] = o[b]; o[b] = u;
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < kThreadTie; ++a) if (a < len) order[i + a] = o[a];
+  } else if (len > kBlockTie) {
+    atomicMax(max_run, (unsigned)len);   // (only the overflow matters to the host)
+  } else if (len > kShortTie) {
+    runs[atomicAdd(run_count, 1u)] = make_int2((int)i, len);
+  }
+  // runs of 3..kShortTie: one list append per warp
+  const bool is_mid = len > kThreadTie && len <= kShortTie;
+  const unsigned m = __ballot_sync(0xffffffffu, is_mid);
+  if (m) {
+    const unsigned lane = threadIdx.x & 31u;
+    const int leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if ((int)lane == leader) base = atomicAdd(mid_count, (unsigned)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (is_mid) mid[base + __popc(m & ((1u << lane) - 1u))] = make_int2((int)i, len);
+  }
 }
 
-// Within each run of equal weights of at most kShortTie edges, order the edges
-// by (u, v) -- one thread per run, insertion sort (the uv keys are distinct).
-__global__ void k_edge_fix_ties(const unsigned long long* __restrict__ w, long long ne,
-                                const unsigned long long* __restrict__ euv, unsigned* __restrict__ order) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i + 1 >= ne || w[i] != w[i + 1] || (i > 0 && w[i - 1] == w[i])) return;
-  int len = 2;
-  while (len <= kShortTie && i + len < ne && w[i + len] == w[i]) ++len;
-  if (len > kShortTie) return;   // a longer run: k_edge_fix_long
-  unsigned o[kShortTie];
-  unsigned long long k[kShortTie];
-  for (int a = 0; a < len; ++a) {
-    o[a] = order[i + a];
-    k[a] = euv[o[a]];
+// A warp per listed run of kThreadTie+1..kShortTie edges: bitonic sort of (uv, edge) across the lanes.
+__global__ void k_edge_fix_mid(const int2* __restrict__ mid, const unsigned* __restrict__ mid_count,
+                               const unsigned long long* __restrict__ euv, unsigned* __restrict__ order) {
+  const unsigned cnt = *mid_count;
+  const int lane = (int)(threadIdx.x & 31u);
+  const unsigned warps = gridDim.x * (blockDim.x >> 5);
+  for (unsigned r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < cnt; r += warps) {
+    const int2 run = mid[r];
+    unsigned o = 0;
+    unsigned long long k = ~0ull;
+    if (lane < run.y) {
+      o = order[run.x + lane];
+      k = euv[o];
+    }
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int j = size >> 1; j > 0; j >>= 1) {
+        const unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, j);
+        const unsigned po = __shfl_xor_sync(0xffffffffu, o, j);
+        const bool lower = (lane & j) == 0;
+        const bool up = (lane & size) == 0;
+        // the lower lane of a pair keeps the min when sorting up, the max otherwise
+        const bool take = lower == up ? pk < k : pk > k;
+        if (take) { k = pk; o = po; }
+      }
+    }
+    if (lane < run.y) order[run.x + lane] = o;
   }
-  for (int a = 1; a < len; ++a) {
-    const unsigned oa = o[a];
-    const unsigned long long ka = k[a];
-    int b = a - 1;
-    while (b >= 0 && k[b] > ka) { k[b + 1] = k[b]; o[b + 1] = o[b]; --b; }
-    k[b + 1] = ka;
-    o[b + 1] = oa;
-  }
-  for (int a = 0; a < len; ++a) order[i + a] = o[a];
 }
 
 // One block per listed run (kShortTie < length <= kBlockTie): bitonic sort of

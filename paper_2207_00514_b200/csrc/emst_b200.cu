@@ -78,7 +78,7 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 }  // namespace
 
 constexpr int kCounters = 16;   // [0] evals [1] scan total [2] err [3] overflow [4] work [5] visits
-                                // [6] found [7] ties [8] frontier size [9] skipped queries [10] big tops
+                                // [6] found [7] ties [8] frontier size [9] skipped queries [10] big tops [11] mid tie runs
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
@@ -137,7 +137,7 @@ struct emst_context {
   DevBuf<long long> out_edges;
   DevBuf<double> out_w;
   DevBuf<double> pairwise;   // total-weight partial sums
-  DevBuf<int2> tie_runs;     // (start, length) of the longer equal-weight runs
+  DevBuf<int2> tie_runs, tie_mid;   // (start, length) of the longer / 3..32-edge equal-weight runs
   long long* host_counters = nullptr;   // pinned mirror of `counters`
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   size_t nodes_stride = 0;
@@ -549,8 +549,12 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
   long long* tie = dev_counter(c, 7);   // low word: longest run, high word: listed long runs
   CK(cudaMemsetAsync(tie, 0, sizeof(long long), c->stream));
   c->tie_runs.ensure(ne / (kShortTie + 1) + 1);
-  launch(c, k_edge_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne, (unsigned*)tie, c->tie_runs.p,
-         (unsigned*)tie + 1);
+  unsigned* mid_n = reinterpret_cast<unsigned*>(dev_counter(c, 11));
+  CK(cudaMemsetAsync(mid_n, 0, sizeof(long long), c->stream));
+  c->tie_mid.ensure(ne / 3 + 1);
+  launch(c, k_edge_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne,
+         (const unsigned long long*)c->euv.p, order, (unsigned*)tie, c->tie_runs.p, (unsigned*)tie + 1, c->tie_mid.p,
+         mid_n);
   read_counters(c);
   const unsigned max_run = (unsigned)(c->host_counters[7] & 0xffffffffll);
   const unsigned long_runs = (unsigned)((unsigned long long)c->host_counters[7] >> 32);
@@ -566,12 +570,15 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
     radix_sort(c, ne, 64, kin, order, false, keys, vin_alt, &keys2, &order2);
     keys = keys2;
     order = order2;
-  } else if (max_run > 1) {
-    launch(c, k_edge_fix_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne,
-           (const unsigned long long*)c->euv.p, order);
-    if (long_runs)
-      launch(c, k_edge_fix_long, long_runs, 1024, 0, (const int2*)c->tie_runs.p, (const unsigned long long*)c->euv.p,
-             order);
+  } else {
+    const unsigned mids = (unsigned)(c->host_counters[11] & 0xffffffffll);
+    if (mids)   // a warp per run
+      launch(c, k_edge_fix_mid, (mids + 7) / 8, 256, 0, (const int2*)c->tie_mid.p, (const unsigned*)mid_n,
+             (const unsigned long long*)c->euv.p, order);
+  }
+  if (max_run <= (unsigned)kBlockTie && long_runs) {
+    launch(c, k_edge_fix_long, long_runs, 1024, 0, (const int2*)c->tie_runs.p, (const unsigned long long*)c->euv.p,
+           order);
   }
   launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, (const unsigned*)order,
          (const unsigned long long*)c->euv.p, ne, edges_dst, w_dst);
@@ -856,7 +863,7 @@ int emst_context_destroy(emst_context* c) {
   c->front[0].release(); c->front[1].release(); c->core_slot.release(); c->core_tmp.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
-  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release();
+  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release(); c->tie_mid.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
