@@ -17,9 +17,15 @@
 
 namespace emst {
 
-constexpr int kSortThreads = 256;
+#ifndef EMST_SORT_THREADS
+#define EMST_SORT_THREADS 256
+#endif
+#ifndef EMST_SORT_ITEMS
+#define EMST_SORT_ITEMS 16
+#endif
+constexpr int kSortThreads = EMST_SORT_THREADS;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 16;
+constexpr int kSortItems = EMST_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys
 constexpr int kRadixBits = 8;
 constexpr int kRadix = 1 << kRadixBits;
@@ -91,7 +97,7 @@ __device__ __forceinline__ unsigned warp_incl_sum_u32(unsigned v) {
 }
 
 #ifndef EMST_SORT_MINB
-#define EMST_SORT_MINB 3
+#define EMST_SORT_MINB 4
 #endif
 
 // One counting-sort pass over `shift`'s 8-bit digit.  Per tile of 4096 keys:
