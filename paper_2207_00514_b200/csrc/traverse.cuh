@@ -130,6 +130,13 @@ constexpr int kTraverseThreads = 256;
 #ifndef EMST_SMEM_STACK
 #define EMST_SMEM_STACK 12
 #endif
+#ifndef EMST_TRAV_PREFETCH
+#define EMST_TRAV_PREFETCH 8192
+#endif
+#ifndef EMST_TRAV_PF_STAGE
+#define EMST_TRAV_PF_STAGE 1
+#endif
+constexpr long long kTravPrefetch = EMST_TRAV_PREFETCH;   // L2 prefetch lookahead in slots (0: off)
 constexpr int kTraverseChunk = EMST_TRAV_CHUNK;   // consecutive Morton queries a warp claims at once
 constexpr int kSmemStack = EMST_SMEM_STACK;       // stack entries per lane kept in shared memory
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
@@ -371,7 +378,31 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       if (done) finalize();
       if (pool_next >= pool_end && !exhausted) {
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(work_counter, (unsigned long long)kTraverseChunk);
+        if (lane == 0) {
+          base = atomicAdd(work_counter, (unsigned long long)kTraverseChunk);
+#if EMST_TRAV_PREFETCH
+          // Warm L2 for the queries kTravPrefetch slots ahead: the low tree levels
+          // they start in are the node records of about the same indices (Karras
+          // numbering), and first touches of those are the traversal's DRAM reads.
+          const long long a = q0 + (long long)base + kTravPrefetch;
+          if (a + kTraverseChunk < q1) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         :: "l"(nodes + a), "r"((unsigned)(kTraverseChunk * sizeof(*nodes))) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         :: "l"(spts + a), "r"((unsigned)(kTraverseChunk * sizeof(float4))) : "memory");
+#if EMST_TRAV_PF_STAGE
+            // the per-slot words the chunk staging loads (4-byte arrays: 16-byte aligned when a is a multiple of 4)
+            if ((a & 3) == 0) {
+              const unsigned bytes = (unsigned)(kTraverseChunk * sizeof(int));
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(label + a), "r"(bytes) : "memory");
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(leaf_parent + a), "r"(bytes) : "memory");
+              if (kBounds) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(nfn_lb + a), "r"(bytes) : "memory");
+              if (top_pure) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(top_pure + a), "r"(bytes) : "memory");
+            }
+#endif
+          }
+#endif
+        }
         base = __shfl_sync(0xffffffffu, base, 0);
         if ((long long)base >= total) {
           exhausted = true;
