@@ -94,7 +94,20 @@ k_core(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restr
     if (n_idle >= 16) {
       if (pool_next >= pool_end && !exhausted) {
         unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(work_counter, (unsigned long long)kCoreChunk);
+        if (lane == 0) {
+          base = atomicAdd(work_counter, (unsigned long long)kCoreChunk);
+#if EMST_TRAV_PREFETCH
+          const long long a = q0 + (long long)base + kTravPrefetch;   // (as in k_traverse)
+          if (a + kCoreChunk < q1) {
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         :: "l"(nodes + a), "r"((unsigned)(kCoreChunk * sizeof(*nodes))) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         :: "l"(spts + a), "r"((unsigned)(kCoreChunk * sizeof(float4))) : "memory");
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         :: "l"(up + a), "r"((unsigned)(kCoreChunk * sizeof(int2))) : "memory");
+          }
+#endif
+        }
         base = __shfl_sync(0xffffffffu, base, 0);
         if ((long long)base >= total) {
           exhausted = true;

@@ -399,6 +399,8 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
               if (kBounds) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(nfn_lb + a), "r"(bytes) : "memory");
               if (top_pure) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(top_pure + a), "r"(bytes) : "memory");
             }
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                         :: "l"(up + a), "r"((unsigned)(kTraverseChunk * sizeof(int2))) : "memory");
 #endif
           }
 #endif
