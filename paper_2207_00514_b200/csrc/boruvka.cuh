@@ -300,9 +300,11 @@ __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __rest
       const int bg = bprefix[gamma], bg1 = bprefix[gamma + 1];
       lab.x = bg == bl ? label[r.x] : kMixed;
       lab.y = bh == bg1 ? label[r.y] : kMixed;
+      // only a child that just turned pure is a new top pure node: one that was
+      // already pure keeps its top[] entries from the round it turned pure
       if (top) {
-        if (refs.x >= 0 && lab.x != kMixed) mark_top(refs.x, r.x, gamma, top, big, big_count);
-        if (refs.y >= 0 && lab.y != kMixed) mark_top(refs.y, gamma + 1, r.y, top, big, big_count);
+        if (refs.x >= 0 && lab.x != kMixed && ref4.z == kMixed) mark_top(refs.x, r.x, gamma, top, big, big_count);
+        if (refs.y >= 0 && lab.y != kMixed && ref4.w == kMixed) mark_top(refs.y, gamma + 1, r.y, top, big, big_count);
       }
     }
     // (a node that stays mixed with mixed children -- most of them early on --
