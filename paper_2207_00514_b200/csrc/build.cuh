@@ -91,6 +91,7 @@ k_scene(const float* __restrict__ pts, long long n, float* __restrict__ part_lo,
     double ext = __dsub_rn((double)h, (double)l);
     scene->lo[k] = (double)l;
     scene->inv[k] = ext > 0.0 ? __drcp_rn(ext) : 0.0;   // IEEE 1/ext (geometry.py:205)
+    scene->cellw[k] = ext > 0.0 ? __drcp_rn(scene->inv[k] * (D == 3 ? 2097152.0 : 2147483648.0)) : 0.0;
   }
   scene->blocks_done = 0;
 }

@@ -121,6 +121,7 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 struct Scene {
   double lo[3];
   double inv[3];
+  double cellw[3];       // world width of one finest lattice cell per axis (0: zero extent)
   float flo[3];
   float fhi[3];
   long long bad_row;     // first row holding a non-finite coordinate, or LLONG_MAX
@@ -193,6 +194,36 @@ __device__ __forceinline__ int ball_prefix(const float* q, double r, const Scene
     prefix = x ? min(prefix, pk) : prefix;
   }
   return prefix;
+}
+
+// Lower bound of the distance from q to any point OUTSIDE the Karras node whose
+// Morton prefix has length `pl` (q's own leaf lies under it): such a point's
+// code differs from q's within the first pl bits, so on some axis whose bits
+// the prefix fixes its lattice cell lies outside q's cell block on that axis.
+// The distance to the block's faces loses one finest cell of slack, far more
+// than any f64 rounding of the quantiser or of this arithmetic.  pl < 0: the root (no outside).
+template <int D>
+__device__ __forceinline__ double cell_exterior(const float* q, int pl, const Scene& sc) {
+  constexpr int bits = D == 3 ? 21 : 31;
+  const double scale = D == 3 ? 2097152.0 : 2147483648.0;
+  double best = __longlong_as_double(0x7ff0000000000000ll);
+  if (pl < 0) return best;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const int t = pl - (64 - D * bits) - k;   // code positions of axis k inside the prefix: off + D*j + k < pl
+    const int bk = t > 0 ? min(bits, (t + D - 1) / D) : 0;
+    const double w = sc.cellw[k];   // one finest cell
+    if (bk == 0 || !(w > 0.0)) continue;
+    const unsigned long long cq = lattice_cell_d((double)q[k], sc.lo[k], sc.inv[k], scale);
+    const int sh = bits - bk;
+    const unsigned long long c0 = (cq >> sh) << sh, c1 = c0 + (1ull << sh);
+    // (offsets from lo, all <= the extent: rounding stays ~1e-15 of the extent,
+    // against a slack of one cell, >= 2^-31 of it)
+    const double dq = (double)q[k] - sc.lo[k];
+    if (c0 > 0) best = fmin(best, dq - (double)c0 * w - w);
+    if (c1 < (1ull << bits)) best = fmin(best, (double)c1 * w - dq - w);
+  }
+  return fmax(best, 0.0);
 }
 
 }  // namespace emst

@@ -87,6 +87,7 @@ struct emst_context {
   int seed_window = 8;            // extra Z-order seed pairs (s +- 2..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
   long long round_comps = 0;      // components entering the running round
   int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
+  int proof_from = 3;             // first round whose traversal records the full nearest-foreign proof (EMST_PROOF_FROM)
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
@@ -440,11 +441,11 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   }
 }
 
-template <int D, bool S, bool B, bool M>
+template <int D, bool S, bool B, bool M, bool P>
 void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1) {
   if (q1 <= q0) return;
   using Node = typename NodeOf<D>::type;
-  auto kernel = k_traverse<D, S, B, M>;
+  auto kernel = k_traverse<D, S, B, M, P>;
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTraverseThreads, 0));
   const long long warps_needed = (q1 - q0 + kTraverseChunk - 1) / kTraverseChunk;
@@ -473,8 +474,9 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
 
 template <int D, bool S, bool B>
 void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
-  if (c->core) traverse_range_m<D, S, B, true>(c, out, q0, q1);
-  else traverse_range_m<D, S, B, false>(c, out, q0, q1);
+  if (c->core) traverse_range_m<D, S, B, true, false>(c, out, q0, q1);
+  else if (B && c->round >= c->proof_from && c->proof_from > 0) traverse_range_m<D, S, B, false, B>(c, out, q0, q1);
+  else traverse_range_m<D, S, B, false, false>(c, out, q0, q1);
 }
 
 void traverse_dispatch(emst_context* c, int flags, EdgeKey* out, long long q0, long long q1) {
@@ -823,6 +825,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     c->device = device;
     if (const char* t = getenv("EMST_SEED_WINDOW")) c->seed_window = atoi(t);
     if (const char* t = getenv("EMST_SEED_FROM")) c->seed_from = atoi(t);
+    if (const char* t = getenv("EMST_PROOF_FROM")) c->proof_from = atoi(t);
     c->rank = rank;
     c->world = world;
     set_device(c);

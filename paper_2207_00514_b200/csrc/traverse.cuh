@@ -198,11 +198,12 @@ struct Pending {
 // box is pruned only when its lower bound is strictly above r2 (ties at the
 // radius are kept, mst.py:259/282/296).  Returns true when an internal child
 // should be explored (lb in *lb_out).
-template <int D, bool kSkip, bool kBounds, class Rec>
+template <int D, bool kSkip, bool kBounds, bool kProof, class Rec>
 __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const float* q, unsigned qp, int comp,
                                             float& r2, Pending& pend, const float4* __restrict__ spts,
                                             unsigned long long* ub, bool share, unsigned& evals, float lb,
-                                            bool enabled, const double* __restrict__ core, double cq) {
+                                            bool enabled, const double* __restrict__ core, double cq,
+                                            float& pmin2) {
   const int c = side ? rec.ref.y : rec.ref.x;
   const int cl = side ? rec.ref.w : rec.ref.z;
   const bool same = cl == comp && (c < 0 || kSkip);
@@ -262,7 +263,10 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
 // out [depth][thread] (bank = lane for every depth, so lanes at different depths
 // never conflict); deeper entries, rare, spill to a per-thread local array up to
 // the reference's capacity of 64 (bvh.py:36).
-template <int D, bool kSkip, bool kBounds, bool kMrd>
+// kProof: record the search's full nearest-foreign proof (pruned lower bounds
+// and the stop node's cell, see cell_exterior) instead of just the radius; it
+// lets later rounds settle more queries up front, and costs a little per visit.
+template <int D, bool kSkip, bool kBounds, bool kMrd, bool kProof>
 __global__ void __launch_bounds__(kTraverseThreads, D == 3 ? EMST_TRAV_MINB3 : EMST_TRAV_MINB2)
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
@@ -311,6 +315,12 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   int prefix = 0;          // Morton prefix shared by the search box
   float prefix_r2 = 0.f;   // r2 `prefix` was computed for
   int since_refresh = 0;
+  // nearest-foreign proof of the search: the smallest lower bound of anything it
+  // pruned, and the prefix length of the node its climb stopped at (everything
+  // outside that node is at least cell_exterior away); -1: the climb reached the
+  // root, -2: the query was settled without a search
+  float pmin2 = 0.f;
+  int stop_pl = -2;
   unsigned evals = 0, visits = 0, found = 0, skipped = 0;
   // A finished query keeps its state until the warp refills: the exact weight
   // of its candidate, the nearest-foreign bound and the 128-bit atomic min then
@@ -320,6 +330,8 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   auto finalize = [&]() {
     unsigned long long w = ~0ull, uv = ~0ull;
     double proven = radius;
+    if (kProof && stop_pl != -2)
+      proven = fmin(cell_exterior<D>(q, stop_pl, sc), (double)__fsqrt_rd(pmin2));
     if (pend.slot >= 0) {
       exact_key<D>(q, qp, spts, pend.slot, w, uv, core, cq);
       const double wd = __longlong_as_double((long long)w);
@@ -458,6 +470,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           prefix = radius < 1e300 ? ball_prefix<D>(q, radius, sc) : -1;
           prefix_r2 = r2;
           since_refresh = kRadiusRefresh / 2;   // staged radius may be stale: refresh early
+          pmin2 = __int_as_float(0x7f800000);
           my_nlb = kBounds ? s_nlb[wib][k] : 0.f;
           // A previous round proved every foreign point is farther than nfn_lb[s]
           // (foreign sets only shrink, so that stays true).  If that already
@@ -484,6 +497,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
             }
           }
           skipped += climb < 0;
+          stop_pl = climb < 0 ? -2 : -1;
         }
       }
     }
@@ -503,6 +517,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     while (top > 0) {
       e = stk_get(top - 1);
       if (__int_as_float(e.y) <= r2) break;
+      if (kProof) pmin2 = fminf(pmin2, __int_as_float(e.y));
       --top;
       e.x = -1;
     }
@@ -524,16 +539,25 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       if (climbing) u = __ldg(up + node);   // (parent link, prefix length of `climb`)
       float lb0, lb1;
       node_lb2(rec, q, lb0, lb1);
-      const bool w0 = visit_child<D, kSkip, kBounds>(rec, 0, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
-                                                     lb0, sides & 1u, core, cq);
-      const bool w1 = visit_child<D, kSkip, kBounds>(rec, 1, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
-                                                     lb1, sides & 2u, core, cq);
+      const bool w0 = visit_child<D, kSkip, kBounds, kProof>(rec, 0, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
+                                                     lb0, sides & 1u, core, cq, pmin2);
+      const bool w1 = visit_child<D, kSkip, kBounds, kProof>(rec, 1, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
+                                                     lb1, sides & 2u, core, cq, pmin2);
       const bool want0 = w0 && lb0 <= r2, want1 = w1 && lb1 <= r2;
+      // (a child the other one's candidate has since put beyond r2 is pruned too)
+      if (kProof) {
+        // every foreign (or mixed) child not pushed, pruned or a leaf already
+        // tested: nothing in it is nearer than its lower bound
+        const bool f0 = (sides & 1u) && !want0 && !(rec.ref.z == comp && (rec.ref.x < 0 || kSkip));
+        const bool f1 = (sides & 2u) && !want1 && !(rec.ref.w == comp && (rec.ref.y < 0 || kSkip));
+        pmin2 = fminf(pmin2, fminf(f0 ? lb0 : __int_as_float(0x7f800000), f1 ? lb1 : __int_as_float(0x7f800000)));
+      }
       const int np = (int)want0 + (int)want1;
       if (top + np > kStackCapacity) {
         atomicOr(overflow, 1);
         top = 0;
         climb = -1;
+        stop_pl = -2;
       } else if (np == 2) {
         // nearer child on top (popped first); ties keep the left child there
         const bool near1 = lb1 < lb0;
@@ -555,6 +579,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           prefix_r2 = r2;
         }
         if (u.y <= prefix || u.x < 0) {
+          stop_pl = u.x < 0 ? -1 : u.y;
           climb = -1;   // every point within the radius lies under this ancestor
         } else {
           climb = u.x >> 1;
