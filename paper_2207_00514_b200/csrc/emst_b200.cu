@@ -87,6 +87,7 @@ struct emst_context {
   int seed_window = 8;            // extra Z-order seed pairs (s +- 2..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
   long long round_comps = 0;      // components entering the running round
   int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
+  bool trace = false;             // per-round trace on stderr (EMST_TRACE=1; developer aid)
   int proof_from = 3;             // first round whose traversal records the full nearest-foreign proof (EMST_PROOF_FROM)
   ncclComm_t comm = nullptr;
   cudaStream_t stream = nullptr;
@@ -438,6 +439,7 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
     read_counters(c);
     c->front_n = (long long)(unsigned)c->host_counters[8];
     c->front_pending = false;
+    if (c->trace) fprintf(stderr, "[emst] round %d comps %lld: %lld nodes still mixed\n", c->round, c->round_comps, c->front_n);
   }
 }
 
@@ -469,6 +471,7 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
   CK(cudaEventElapsedTime(&ms, c->tv_a, c->tv_b));
   c->traverse_ms += ms;
   c->traverse_launches++;
+  if (c->trace) fprintf(stderr, "[emst] round %d traverse [%lld, %lld): %.3f ms\n", c->round, q0, q1, ms);
   c->traverse_queries += q1 - q0;
 }
 
@@ -826,6 +829,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (const char* t = getenv("EMST_SEED_WINDOW")) c->seed_window = atoi(t);
     if (const char* t = getenv("EMST_SEED_FROM")) c->seed_from = atoi(t);
     if (const char* t = getenv("EMST_PROOF_FROM")) c->proof_from = atoi(t);
+    if (const char* t = getenv("EMST_TRACE")) c->trace = atoi(t) != 0;
     c->rank = rank;
     c->world = world;
     set_device(c);
