@@ -211,3 +211,27 @@ def test_massive_ties_match_oracle(case):
     ref = orc.boruvka_emst(pts)
     assert np.array_equal(res.edges, ref.edges) and np.array_equal(res.weights, ref.weights), case
     assert res.iterations == ref.iterations and list(res.component_counts) == list(ref.component_counts)
+
+
+@pytest.mark.parametrize("env", [{"EMST_PROOF_FROM": "0"}, {"EMST_PROOF_FROM": "1"}, {"EMST_PROOF_FROM": "2"},
+                                 {"EMST_SEED_WINDOW": "0"}, {"EMST_SEED_WINDOW": "24", "EMST_SEED_FROM": "1"}])
+def test_search_switches_do_not_change_the_result(env, monkeypatch):
+    """The work-only switches of the solve (nearest-foreign proof from round k, Z-window radius seeds) must
+    leave edges, weights, iterations and counts bit-identical: every bound they add is admissible."""
+    from oracle import oracle as orc
+    g = np.arange(40, dtype=np.float32) / 4
+    lattice = np.stack(np.meshgrid(g, g, indexing="ij"), -1).reshape(-1, 2)
+    clouds = [E.generate(E.DatasetSpec("blobs", 60_000, 3, seed=3)),
+              E.generate(E.DatasetSpec("uniform", 60_000, 2, seed=4)),
+              E.generate(E.DatasetSpec("normal", 60_000, 3, seed=5)), lattice]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    ctx = E._lib.Context(0)
+    try:
+        for pts in clouds:
+            got = E.boruvka_emst(pts, context=ctx)
+            ref = orc.boruvka_emst(pts)
+            assert np.array_equal(got.edges, ref.edges) and np.array_equal(got.weights, ref.weights), env
+            assert got.iterations == ref.iterations and list(got.component_counts) == list(ref.component_counts)
+    finally:
+        ctx.close()
