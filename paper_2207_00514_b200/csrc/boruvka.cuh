@@ -321,6 +321,29 @@ __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __rest
   }
 }
 
+// slots whose label is `value` (warp-aggregated)
+__global__ void k_count_label(const int* __restrict__ label, long long n, int value, unsigned long long* __restrict__ out) {
+  unsigned long long cnt = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    cnt += label[i] == value;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31u) == 0 && cnt) atomicAdd(out, cnt);
+}
+
+// the larger of the last two components (slots of component 1 vs n): its queries are not run
+__global__ void k_pick_side(const unsigned long long* __restrict__ count1, long long n, int* __restrict__ side) {
+  if (threadIdx.x == 0) *side = 2 * (long long)*count1 > n ? 1 : 0;
+}
+
+// the two components of the last round share their minimum edge: copy it to the side left out
+__global__ void k_copy_key(EdgeKey* best, const int* __restrict__ side) {
+  if (threadIdx.x == 0) {
+    const int s = *side;
+    best[s] = best[1 - s];
+  }
+}
+
 // ------------------------------------------------------------------- merge
 constexpr int kErrNoEdge = 1;     // mst.py:365-376 / 720-721
 constexpr int kErrChain = 2;      // mst.py:399-400 / 722-723

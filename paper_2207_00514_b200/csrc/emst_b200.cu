@@ -79,6 +79,7 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 
 constexpr int kCounters = 16;   // [0] evals [1] scan total [2] err [3] overflow [4] work [5] visits
                                 // [6] found [7] ties [8] frontier size [9] skipped queries [10] big tops [11] mid tie runs
+                                // [12] slots of component 1 (last round) [13] the component left out
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
@@ -87,6 +88,8 @@ struct emst_context {
   int seed_window = 8;            // extra Z-order seed pairs (s +- 2..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
   long long round_comps = 0;      // components entering the running round
   int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
+  bool one_side = false;          // last round (2 components): run only the smaller component's queries
+  bool last_round_one_side = true;   // EMST_ONE_SIDE=0 turns that off
   bool trace = false;             // per-round trace on stderr (EMST_TRACE=1; developer aid)
   int proof_from = 3;             // first round whose traversal records the full nearest-foreign proof (EMST_PROOF_FROM)
   ncclComm_t comm = nullptr;
@@ -463,7 +466,8 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
            reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1,
            c->nfn_lb.p, (const int2*)c->up.p, (const int*)c->leaf_parent.p, (const Scene*)c->scene.p,
-           c->top_valid ? (const int*)c->top.p : (const int*)nullptr, c->core);
+           c->top_valid ? (const int*)c->top.p : (const int*)nullptr, c->core,
+           c->one_side ? (const int*)dev_counter(c, 13) : (const int*)nullptr);
   }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
@@ -498,7 +502,15 @@ void traverse_dispatch(emst_context* c, int flags, EdgeKey* out, long long q0, l
 }
 
 // Phase 3: per-component minimum outgoing edge into c->best[0, comps).
+// With two components left, both minima are the same edge (the lightest of the
+// edges between them under (w, u, v)), so only the smaller component's queries
+// run and its key is copied to the other (c->one_side).
+void round_find_all(emst_context* c, long long n, long long comps, int flags);
 void round_find(emst_context* c, long long n, long long comps, int flags) {
+  round_find_all(c, n, comps, flags);
+  if (c->one_side) launch(c, k_copy_key, 1, 32, 0, c->best.p, (const int*)dev_counter(c, 13));
+}
+void round_find_all(emst_context* c, long long n, long long comps, int flags) {
   if (c->vshards > 1) {
     const int V = c->vshards;
     c->shard_keys.ensure((size_t)V * comps);
@@ -703,6 +715,14 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     CK(cudaMemsetAsync(c->best.p, 0xff, comps * sizeof(EdgeKey), c->stream));
     c->round = st->iterations;
     c->round_comps = comps;
+    c->one_side = comps == 2 && c->last_round_one_side;
+    if (c->one_side) {
+      // the component with more slots is the one left out (picked on the device: no host sync)
+      CK(cudaMemsetAsync(dev_counter(c, 12), 0, sizeof(long long), c->stream));
+      launch(c, k_count_label, (unsigned)c->num_sms * 4, 256, 0, (const int*)c->label.p, n, 1,
+             reinterpret_cast<unsigned long long*>(dev_counter(c, 12)));
+      launch(c, k_pick_side, 1, 32, 0, (const unsigned long long*)dev_counter(c, 12), n, (int*)dev_counter(c, 13));
+    }
     {
       const bool skip = flags & EMST_SUBTREE_SKIP;
       const LabelMode mode = comps == n ? kLabelsNone : skip ? kLabelsFrontier : kLabelsFull;
@@ -711,6 +731,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     CK(cudaEventRecord(c->ev_a, c->stream));
     c->singleton_round = comps == n;
     round_find(c, n, comps, flags);
+    c->one_side = false;
     c->singleton_round = false;
     c->round = 0;
     CK(cudaEventRecord(c->ev_b, c->stream));
@@ -830,6 +851,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (const char* t = getenv("EMST_SEED_FROM")) c->seed_from = atoi(t);
     if (const char* t = getenv("EMST_PROOF_FROM")) c->proof_from = atoi(t);
     if (const char* t = getenv("EMST_TRACE")) c->trace = atoi(t) != 0;
+    if (const char* t = getenv("EMST_ONE_SIDE")) c->last_round_one_side = atoi(t) != 0;
     c->rank = rank;
     c->world = world;
     set_device(c);
@@ -1225,6 +1247,7 @@ int emst_find_component_outgoing_edges(emst_context* c, const float* pts, int64_
     CK(cudaMemsetAsync(c->best.p, 0xff, n * sizeof(EdgeKey), c->stream));
     CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
     prepare_cores(c, n, 1, core);
+    c->one_side = false;
     round_find(c, n, n, flags);
     c->core = nullptr;
     std::vector<EdgeKey> keys(n);

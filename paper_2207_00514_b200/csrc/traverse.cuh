@@ -274,13 +274,14 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
            unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb,
            const int2* __restrict__ up, const int* __restrict__ leaf_parent, const Scene* __restrict__ scene_ptr,
-           const int* __restrict__ top_pure, const double* __restrict__ core_in) {
+           const int* __restrict__ top_pure, const double* __restrict__ core_in, const int* __restrict__ side) {
   // mutual reachability (kMrd): core distances per slot; compiled out otherwise
   const double* __restrict__ core = kMrd ? core_in : nullptr;
   const unsigned lane = lane_id();
   const unsigned lt = lanemask_lt_u32();
   const int total = (int)(q1 - q0);
   const Scene sc = *scene_ptr;
+  const int skip_comp = side ? *side : -1;   // last round: the component whose queries are not run
 
   // The warp claims kTraverseChunk consecutive Morton slots at a time and stages
   // their point, label, leaf parent, starting radius, proven nearest-foreign
@@ -476,6 +477,8 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           // (foreign sets only shrink, so that stays true).  If that already
           // exceeds the radius, this query cannot find an edge: done.
           if (kBounds && (double)my_nlb > radius) climb = -1;
+          // last round: the other component's queries find the same edge
+          if (comp == skip_comp) climb = -1;
           // mutual reachability: every edge of q weighs at least core(q)
           if (core) {
             cq = __ldg(core + q0 + s);
