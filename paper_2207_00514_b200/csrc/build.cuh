@@ -149,8 +149,31 @@ k_gather(const float* __restrict__ pts, long long n, const unsigned* __restrict_
     if (s < n) {
       spts[s] = v[j];
       perm[s] = p[j];
-      iperm[p[j]] = (unsigned)s;
+      if (iperm) iperm[p[j]] = (unsigned)s;
     }
+  }
+}
+
+// iperm[perm[s]] = s for the targets p in [lo, hi): the random 4-byte scatter
+// runs over one part of iperm at a time, small enough to stay in L2 until its
+// sectors are complete (one pass over all 148 MB at 37M scatters straight to DRAM
+// and costs 1.3 ms of partial-sector writes).  perm is read once per part.
+__global__ void __launch_bounds__(256) k_inverse_perm(const unsigned* __restrict__ perm, long long n, unsigned lo,
+                                                      unsigned hi, unsigned* __restrict__ iperm) {
+  const long long n4 = n >> 2;
+  const uint4* p4 = reinterpret_cast<const uint4*>(perm);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const uint4 v = __ldg(p4 + i);
+    const unsigned s = (unsigned)(i << 2);
+    if (v.x - lo < hi - lo) iperm[v.x] = s;
+    if (v.y - lo < hi - lo) iperm[v.y] = s + 1;
+    if (v.z - lo < hi - lo) iperm[v.z] = s + 2;
+    if (v.w - lo < hi - lo) iperm[v.w] = s + 3;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (n & 3)) {
+    const long long s = (n4 << 2) + threadIdx.x;
+    const unsigned v = perm[s];
+    if (v - lo < hi - lo) iperm[v] = (unsigned)s;
   }
 }
 

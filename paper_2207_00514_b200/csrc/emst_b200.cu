@@ -77,6 +77,7 @@ inline unsigned grid_for(long long n, int threads) { return (unsigned)std::max<l
 
 }  // namespace
 
+constexpr long long kIpermPart = 1ll << 23;   // inverse-permutation targets per scatter part (32 MB of iperm)
 constexpr int kCounters = 16;   // [0] evals [1] scan total [2] err [3] overflow [4] work [5] visits
                                 // [6] found [7] ties [8] frontier size [9] skipped queries [10] big tops [11] mid tie runs
                                 // [12] slots of component 1 (last round) [13] the component left out
@@ -88,6 +89,7 @@ struct emst_context {
   int seed_window = 8;            // extra Z-order seed pairs (s +- 2..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
   long long round_comps = 0;      // components entering the running round
   int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
+  int iperm_parts = 0;            // parts of the inverse-permutation scatter (0: by size, EMST_IPERM_PARTS)
   bool one_side = false;          // last round (2 components): run only the smaller component's queries
   bool last_round_one_side = true;   // EMST_ONE_SIDE=0 turns that off
   bool trace = false;             // per-round trace on stderr (EMST_TRACE=1; developer aid)
@@ -301,8 +303,17 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
   // sorted codes -> k-buffer `skeys`, permutation -> `svals`
   {
     const unsigned g = grid_for(n, kGatherThreads * kGatherPer);
-    if (d == 3) launch(c, k_gather<3>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, c->iperm.p);
-    else launch(c, k_gather<2>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, c->iperm.p);
+    // the inverse permutation: in the gather for small n, else by parts of <= kIpermPart targets
+    const int parts = c->iperm_parts > 0 ? c->iperm_parts : (int)((n + kIpermPart - 1) / kIpermPart);
+    unsigned* ip = parts <= 1 ? c->iperm.p : nullptr;
+    if (d == 3) launch(c, k_gather<3>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, ip);
+    else launch(c, k_gather<2>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, ip);
+    if (!ip) {
+      for (int k = 0; k < parts; ++k) {
+        const unsigned lo = (unsigned)(k * n / parts), hi = (unsigned)((k + 1) * n / parts);
+        launch(c, k_inverse_perm, (unsigned)c->num_sms * 8, 256, 0, (const unsigned*)c->perm.p, n, lo, hi, c->iperm.p);
+      }
+    }
   }
   if (n > 1) {
     const long long m = n - 1;
@@ -852,6 +863,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (const char* t = getenv("EMST_PROOF_FROM")) c->proof_from = atoi(t);
     if (const char* t = getenv("EMST_TRACE")) c->trace = atoi(t) != 0;
     if (const char* t = getenv("EMST_ONE_SIDE")) c->last_round_one_side = atoi(t) != 0;
+    if (const char* t = getenv("EMST_IPERM_PARTS")) c->iperm_parts = atoi(t);
     c->rank = rank;
     c->world = world;
     set_device(c);
