@@ -81,6 +81,7 @@ constexpr long long kIpermPart = 1ll << 23;   // inverse-permutation targets per
 constexpr int kCounters = 16;   // [0] evals [1] scan total [2] err [3] overflow [4] work [5] visits
                                 // [6] found [7] ties [8] frontier size [9] skipped queries [10] big tops [11] mid tie runs
                                 // [12] slots of component 1 (last round) [13] the component left out
+                                // [14] slots listed by the prefilter
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
@@ -89,6 +90,9 @@ struct emst_context {
   int seed_window = 8;            // extra Z-order seed pairs (s +- 2..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
   long long round_comps = 0;      // components entering the running round
   int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
+  double skip_frac = 0.0;         // share of last round's queries settled before their first visit
+  double list_skip = 0.1;         // prefilter the queries when last round settled this share up front (EMST_LIST_SKIP)
+  DevBuf<int> qlist;              // slots the prefilter kept
   int iperm_parts = 0;            // parts of the inverse-permutation scatter (0: by size, EMST_IPERM_PARTS)
   bool one_side = false;          // last round (2 components): run only the smaller component's queries
   bool last_round_one_side = true;   // EMST_ONE_SIDE=0 turns that off
@@ -470,15 +474,28 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
                                                                              blocks_needed));
   unsigned long long* work = reinterpret_cast<unsigned long long*>(dev_counter(c, 4));
   CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
+  const int* side = c->one_side ? (const int*)dev_counter(c, 13) : (const int*)nullptr;
+  // late rounds: list the queries that are not settled up front (Euclidean with bounds only)
+  const bool use_list = B && !M && c->round > 1 && c->skip_frac >= c->list_skip;
+  unsigned* qcount = reinterpret_cast<unsigned*>(dev_counter(c, 14));
   CK(cudaEventRecord(c->tv_a, c->stream));
+  if (use_list) {
+    c->qlist.ensure(q1 - q0);
+    CK(cudaMemsetAsync(qcount, 0, sizeof(long long), c->stream));
+    const unsigned pg = (unsigned)std::min<long long>(grid_for(q1 - q0, 256), (long long)c->num_sms * 8);
+    launch(c, k_prefilter<D>, pg, 256, 0, (const float4*)c->spts.p, (const int*)c->label.p,
+           (const unsigned long long*)c->ub.p, (const float*)c->nfn_lb.p,
+           c->top_valid ? (const int*)c->top.p : (const int*)nullptr, (const int2*)c->up.p, (const Scene*)c->scene.p,
+           q0, q1, side, c->qlist.p, qcount, reinterpret_cast<unsigned long long*>(dev_counter(c, 9)));
+  }
   {
     launch(c, kernel, grid, kTraverseThreads, 0, (const Node*)reinterpret_cast<Node*>(c->nodes.p),
            (const float4*)c->spts.p, (const unsigned*)c->perm.p, (const int*)c->label.p, c->ub.p, out, q0, q1,
            (const Box3*)c->root_box.p, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)),
            reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1,
            c->nfn_lb.p, (const int2*)c->up.p, (const int*)c->leaf_parent.p, (const Scene*)c->scene.p,
-           c->top_valid ? (const int*)c->top.p : (const int*)nullptr, c->core,
-           c->one_side ? (const int*)dev_counter(c, 13) : (const int*)nullptr);
+           c->top_valid ? (const int*)c->top.p : (const int*)nullptr, c->core, side,
+           use_list ? (const int*)c->qlist.p : (const int*)nullptr, (const unsigned*)qcount);
   }
   CK(cudaEventRecord(c->tv_b, c->stream));
   CK(cudaEventSynchronize(c->tv_b));
@@ -711,6 +728,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   CK(cudaMemsetAsync(c->nfn_lb.p, 0, n * sizeof(float), c->stream));
   CK(cudaMemsetAsync(c->top.p, 0, n * sizeof(int), c->stream));
   c->front_n = -1;
+  c->skip_frac = 0.0;
   long long comps = n, edges = 0;
   const int max_it = max_iterations(n);
   st->component_counts[0] = n;
@@ -754,6 +772,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
       st->round_node_visits[r] = c->host_counters[5] - visits_before;
       st->round_found[r] = c->host_counters[6] - found_before;
       st->round_skipped[r] = c->host_counters[9] - skipped_before;
+      c->skip_frac = (double)st->round_skipped[r] / (double)std::max<long long>(1, n / std::max(1, c->world));
       skipped_before = c->host_counters[9];
       visits_before = c->host_counters[5];
       found_before = c->host_counters[6];
@@ -864,6 +883,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (const char* t = getenv("EMST_TRACE")) c->trace = atoi(t) != 0;
     if (const char* t = getenv("EMST_ONE_SIDE")) c->last_round_one_side = atoi(t) != 0;
     if (const char* t = getenv("EMST_IPERM_PARTS")) c->iperm_parts = atoi(t);
+    if (const char* t = getenv("EMST_LIST_SKIP")) c->list_skip = atof(t);
     c->rank = rank;
     c->world = world;
     set_device(c);
@@ -901,7 +921,7 @@ int emst_context_destroy(emst_context* c) {
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
   c->node_parent.release(); c->leaf_parent.release(); c->node_delta.release(); c->up.release(); c->arrivals.release(); c->root_box.release();
   c->label.release(); c->bprefix.release(); c->big_tops.release(); c->top.release();
-  c->front[0].release(); c->front[1].release(); c->core_slot.release(); c->core_tmp.release(); c->nfn_lb.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
+  c->front[0].release(); c->front[1].release(); c->core_slot.release(); c->core_tmp.release(); c->nfn_lb.release(); c->qlist.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release(); c->tie_mid.release();

@@ -274,12 +274,14 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
            unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb,
            const int2* __restrict__ up, const int* __restrict__ leaf_parent, const Scene* __restrict__ scene_ptr,
-           const int* __restrict__ top_pure, const double* __restrict__ core_in, const int* __restrict__ side) {
+           const int* __restrict__ top_pure, const double* __restrict__ core_in, const int* __restrict__ side,
+           const int* __restrict__ qlist, const unsigned* __restrict__ qcount) {
+  // qlist: the slots to run (k_prefilter dropped the ones settled up front), else all of [q0, q1)
   // mutual reachability (kMrd): core distances per slot; compiled out otherwise
   const double* __restrict__ core = kMrd ? core_in : nullptr;
   const unsigned lane = lane_id();
   const unsigned lt = lanemask_lt_u32();
-  const int total = (int)(q1 - q0);
+  const int total = qlist ? (int)*qcount : (int)(q1 - q0);
   const Scene sc = *scene_ptr;
   const int skip_comp = side ? *side : -1;   // last round: the component whose queries are not run
 
@@ -293,6 +295,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   __shared__ unsigned long long s_ub[W][kTraverseChunk];
   __shared__ float s_nlb[W][kTraverseChunk];
   __shared__ int s_top[W][kTraverseChunk];
+  __shared__ int s_slot[W][kTraverseChunk];
   __shared__ int2 s_stk[kSmemStack][kTraverseThreads];
   int2 deep[kStackCapacity - kSmemStack];
   const int wib = threadIdx.x >> 5;
@@ -352,7 +355,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     // statement: with core distances the search bounds weights, not distances)
     if (kBounds && !core) {
       const float pr = __double2float_rd(__dmul_rd(proven, 1.0 - 0x1p-40));
-      if (pr > my_nlb) nfn_lb[q0 + s] = pr;
+      if (pr > my_nlb) nfn_lb[s] = pr;
     }
     done = false;
     s = -1;
@@ -397,8 +400,9 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           // Warm L2 for the queries kTravPrefetch slots ahead: the low tree levels
           // they start in are the node records of about the same indices (Karras
           // numbering), and first touches of those are the traversal's DRAM reads.
+          // (not for listed queries: warming the slots around the listed ones measured neutral)
           const long long a = q0 + (long long)base + kTravPrefetch;
-          if (a + kTraverseChunk < q1) {
+          if (!qlist && a + kTraverseChunk < q1) {
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
                          :: "l"(nodes + a), "r"((unsigned)(kTraverseChunk * sizeof(*nodes))) : "memory");
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
@@ -430,7 +434,8 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           for (int j = 0; j < kTraverseChunk / 32; ++j) {
             const int i = chunk_base + j * 32 + (int)lane;
             if (i < pool_end) {
-              const long long g = q0 + i;
+              const long long g = qlist ? (long long)qlist[i] : q0 + i;
+              if (qlist) s_slot[wib][j * 32 + lane] = (int)g;
               s_pts[wib][j * 32 + lane] = spts[g];
               s_lab[wib][j * 32 + lane] = label[g];
               s_lp[wib][j * 32 + lane] = leaf_parent[g];
@@ -455,8 +460,8 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         const bool take = s < 0 && mine < pool_end;
         pool_next = min(pool_end, pool_next + n_idle);
         if (take) {
-          s = mine;
           const int k = mine - chunk_base;
+          s = qlist ? s_slot[wib][k] : (int)(q0 + mine);   // the query's slot
           const float4 qv = s_pts[wib][k];
           q[0] = qv.x; q[1] = qv.y; q[2] = qv.z;
           qp = __float_as_uint(qv.w);
@@ -481,7 +486,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           if (comp == skip_comp) climb = -1;
           // mutual reachability: every edge of q weighs at least core(q)
           if (core) {
-            cq = __ldg(core + q0 + s);
+            cq = __ldg(core + s);
             if (cq > radius) climb = -1;
           }
           // Every leaf under the query's top pure node T is in its own component:
