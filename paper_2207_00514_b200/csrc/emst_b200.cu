@@ -91,6 +91,7 @@ struct emst_context {
   long long round_comps = 0;      // components entering the running round
   int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
   double skip_frac = 0.0;         // share of last round's queries settled before their first visit
+  bool single_kernel = true;      // round 1 runs its own compiled traversal (EMST_SINGLE_KERNEL=0: the general one)
   double list_skip = 0.1;         // prefilter the queries when last round settled this share up front (EMST_LIST_SKIP)
   DevBuf<int> qlist;              // slots the prefilter kept
   int iperm_parts = 0;            // parts of the inverse-permutation scatter (0: by size, EMST_IPERM_PARTS)
@@ -461,11 +462,11 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   }
 }
 
-template <int D, bool S, bool B, bool M, bool P>
+template <int D, bool S, bool B, bool M, bool P, bool G = false>
 void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1) {
   if (q1 <= q0) return;
   using Node = typename NodeOf<D>::type;
-  auto kernel = k_traverse<D, S, B, M, P>;
+  auto kernel = k_traverse<D, S, B, M, P, G>;
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTraverseThreads, 0));
   const long long warps_needed = (q1 - q0 + kTraverseChunk - 1) / kTraverseChunk;
@@ -509,7 +510,9 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
 
 template <int D, bool S, bool B>
 void traverse_range(emst_context* c, EdgeKey* out, long long q0, long long q1) {
+  const bool single = c->singleton_round && c->vshards == 1 && c->world == 1;
   if (c->core) traverse_range_m<D, S, B, true, false>(c, out, q0, q1);
+  else if (single && c->single_kernel) traverse_range_m<D, S, B, false, false, true>(c, out, q0, q1);
   else if (B && c->round >= c->proof_from && c->proof_from > 0) traverse_range_m<D, S, B, false, B>(c, out, q0, q1);
   else traverse_range_m<D, S, B, false, false>(c, out, q0, q1);
 }
@@ -884,6 +887,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (const char* t = getenv("EMST_ONE_SIDE")) c->last_round_one_side = atoi(t) != 0;
     if (const char* t = getenv("EMST_IPERM_PARTS")) c->iperm_parts = atoi(t);
     if (const char* t = getenv("EMST_LIST_SKIP")) c->list_skip = atof(t);
+    if (const char* t = getenv("EMST_SINGLE_KERNEL")) c->single_kernel = atoi(t) != 0;
     c->rank = rank;
     c->world = world;
     set_device(c);

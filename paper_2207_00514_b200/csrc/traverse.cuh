@@ -198,7 +198,7 @@ struct Pending {
 // box is pruned only when its lower bound is strictly above r2 (ties at the
 // radius are kept, mst.py:259/282/296).  Returns true when an internal child
 // should be explored (lb in *lb_out).
-template <int D, bool kSkip, bool kBounds, bool kProof, class Rec>
+template <int D, bool kSkip, bool kBounds, bool kProof, bool kSingle, class Rec>
 __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const float* q, unsigned qp, int comp,
                                             float& r2, Pending& pend, const float4* __restrict__ spts,
                                             unsigned long long* ub, bool share, unsigned& evals, float lb,
@@ -206,7 +206,8 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
                                             float& pmin2) {
   const int c = side ? rec.ref.y : rec.ref.x;
   const int cl = side ? rec.ref.w : rec.ref.z;
-  const bool same = cl == comp && (c < 0 || kSkip);
+  // (round 1: every point is its own component and the query never visits its own leaf)
+  const bool same = !kSingle && cl == comp && (c < 0 || kSkip);
   if (!enabled || same || lb > r2) return false;
   if (c >= 0) return true;
   ++evals;
@@ -266,7 +267,9 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
 // kProof: record the search's full nearest-foreign proof (pruned lower bounds
 // and the stop node's cell, see cell_exterior) instead of just the radius; it
 // lets later rounds settle more queries up front, and costs a little per visit.
-template <int D, bool kSkip, bool kBounds, bool kMrd, bool kProof>
+// kSingle: round 1 compiled on its own (every query its own component, nothing
+// is ever "same component", no shared radius).
+template <int D, bool kSkip, bool kBounds, bool kMrd, bool kProof, bool kSingle>
 __global__ void __launch_bounds__(kTraverseThreads, D == 3 ? EMST_TRAV_MINB3 : EMST_TRAV_MINB2)
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
@@ -274,8 +277,13 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            unsigned long long* __restrict__ evals_out, int* __restrict__ overflow,
            unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb,
            const int2* __restrict__ up, const int* __restrict__ leaf_parent, const Scene* __restrict__ scene_ptr,
-           const int* __restrict__ top_pure, const double* __restrict__ core_in, const int* __restrict__ side,
-           const int* __restrict__ qlist, const unsigned* __restrict__ qcount) {
+           const int* __restrict__ top_pure_in, const double* __restrict__ core_in, const int* __restrict__ side_in,
+           const int* __restrict__ qlist_in, const unsigned* __restrict__ qcount) {
+  // round 1 (kSingle) has no pure nodes, no one-sided round, no query list and no earlier proofs
+  const int* __restrict__ top_pure = kSingle ? nullptr : top_pure_in;
+  const int* __restrict__ side = kSingle ? nullptr : side_in;
+  const int* __restrict__ qlist = kSingle ? nullptr : qlist_in;
+  constexpr bool kNlb = kBounds && !kSingle;
   // qlist: the slots to run (k_prefilter dropped the ones settled up front), else all of [q0, q1)
   // mutual reachability (kMrd): core distances per slot; compiled out otherwise
   const double* __restrict__ core = kMrd ? core_in : nullptr;
@@ -343,7 +351,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       // (a strictly smaller radius means another query already beat this edge)
       if (!(wd > radius)) {
         ++found;
-        if (singletons) {
+        if (kSingle || singletons) {
           store_key(&best[comp], w, uv);   // round 1: the query is its component
         } else {
           if (kBounds && kShareAtEnd && w < __ldcg(&ub[comp])) atomicMin(&ub[comp], w);
@@ -413,7 +421,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
               const unsigned bytes = (unsigned)(kTraverseChunk * sizeof(int));
               asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(label + a), "r"(bytes) : "memory");
               asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(leaf_parent + a), "r"(bytes) : "memory");
-              if (kBounds) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(nfn_lb + a), "r"(bytes) : "memory");
+              if (kNlb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(nfn_lb + a), "r"(bytes) : "memory");
               if (top_pure) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(top_pure + a), "r"(bytes) : "memory");
             }
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
@@ -439,7 +447,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
               s_pts[wib][j * 32 + lane] = spts[g];
               s_lab[wib][j * 32 + lane] = label[g];
               s_lp[wib][j * 32 + lane] = leaf_parent[g];
-              if (kBounds) s_nlb[wib][j * 32 + lane] = nfn_lb[g];
+              if (kNlb) s_nlb[wib][j * 32 + lane] = nfn_lb[g];
               if (top_pure) s_top[wib][j * 32 + lane] = top_pure[g];
             }
           }
@@ -477,11 +485,11 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
           prefix_r2 = r2;
           since_refresh = kRadiusRefresh / 2;   // staged radius may be stale: refresh early
           pmin2 = __int_as_float(0x7f800000);
-          my_nlb = kBounds ? s_nlb[wib][k] : 0.f;
+          my_nlb = kNlb ? s_nlb[wib][k] : 0.f;
           // A previous round proved every foreign point is farther than nfn_lb[s]
           // (foreign sets only shrink, so that stays true).  If that already
           // exceeds the radius, this query cannot find an edge: done.
-          if (kBounds && (double)my_nlb > radius) climb = -1;
+          if (kNlb && (double)my_nlb > radius) climb = -1;
           // last round: the other component's queries find the same edge
           if (comp == skip_comp) climb = -1;
           // mutual reachability: every edge of q weighs at least core(q)
@@ -511,7 +519,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     }
     if (s < 0 || done) continue;
 
-    if (kBounds && !singletons && ++since_refresh >= kRadiusRefresh) {
+    if (kBounds && !(kSingle || singletons) && ++since_refresh >= kRadiusRefresh) {
       since_refresh = 0;
       const double shared = bits_to_radius(__ldcg(&ub[comp]));
       if (shared < radius) { radius = shared; r2 = fminf(r2, prune_r2(shared)); }
@@ -547,9 +555,9 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       if (climbing) u = __ldg(up + node);   // (parent link, prefix length of `climb`)
       float lb0, lb1;
       node_lb2(rec, q, lb0, lb1);
-      const bool w0 = visit_child<D, kSkip, kBounds, kProof>(rec, 0, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
+      const bool w0 = visit_child<D, kSkip, kBounds, kProof, kSingle>(rec, 0, q, qp, comp, r2, pend, spts, ub, !(kSingle || singletons), evals,
                                                      lb0, sides & 1u, core, cq, pmin2);
-      const bool w1 = visit_child<D, kSkip, kBounds, kProof>(rec, 1, q, qp, comp, r2, pend, spts, ub, !singletons, evals,
+      const bool w1 = visit_child<D, kSkip, kBounds, kProof, kSingle>(rec, 1, q, qp, comp, r2, pend, spts, ub, !(kSingle || singletons), evals,
                                                      lb1, sides & 2u, core, cq, pmin2);
       const bool want0 = w0 && lb0 <= r2, want1 = w1 && lb1 <= r2;
       // (a child the other one's candidate has since put beyond r2 is pruned too)

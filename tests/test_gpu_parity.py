@@ -215,7 +215,8 @@ def test_massive_ties_match_oracle(case):
 
 @pytest.mark.parametrize("env", [{"EMST_PROOF_FROM": "0"}, {"EMST_PROOF_FROM": "1"}, {"EMST_PROOF_FROM": "2"},
                                  {"EMST_SEED_WINDOW": "0"}, {"EMST_SEED_WINDOW": "24", "EMST_SEED_FROM": "1"},
-                                 {"EMST_ONE_SIDE": "0"}, {"EMST_LIST_SKIP": "0"}, {"EMST_LIST_SKIP": "2"}])
+                                 {"EMST_ONE_SIDE": "0"}, {"EMST_LIST_SKIP": "0"}, {"EMST_LIST_SKIP": "2"},
+                                 {"EMST_SINGLE_KERNEL": "0"}])
 def test_search_switches_do_not_change_the_result(env, monkeypatch):
     """The work-only switches of the solve (nearest-foreign proof from round k, Z-window radius seeds, one
     side of the last round, prefiltered query lists) must
