@@ -105,7 +105,6 @@ struct emst_context {
   long long launches = 0;
   double traverse_ms = 0.0;
   long long traverse_launches = 0, traverse_queries = 0;
-  cudaEvent_t tv_a = nullptr, tv_b = nullptr;
   int num_sms = 148;
 
   // build
@@ -152,6 +151,19 @@ struct emst_context {
   DevBuf<int2> tie_runs, tie_mid;   // (start, length) of the longer / 3..32-edge equal-weight runs
   long long* host_counters = nullptr;   // pinned mirror of `counters`
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // Phase timers read back lazily: event pairs are recorded on the stream and
+  // their times collected at the next stream sync the solve needs anyway (the
+  // round's counter read), so timing adds no host round trip of its own.
+  struct Timer {
+    cudaEvent_t a, b;
+    double* acc;      // += elapsed ms (or nullptr)
+    bool trav;        // a traversal launch (traverse_ms, trace)
+    int round;
+    long long q0, q1;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  std::vector<Timer> timers;
   size_t nodes_stride = 0;
   int dim = 0;
   long long n = 0;
@@ -170,9 +182,41 @@ void launch(emst_context* c, K kernel, unsigned grid, unsigned block, size_t sme
 
 long long* dev_counter(emst_context* c, int i) { return c->counters.p + i; }
 
+cudaEvent_t timer_event(emst_context* c) {
+  if (c->ev_next == c->ev_pool.size()) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    c->ev_pool.push_back(e);
+  }
+  cudaEvent_t e = c->ev_pool[c->ev_next++];
+  CK(cudaEventRecord(e, c->stream));
+  return e;
+}
+
+// collect every recorded timer (call after a stream sync: all their events are complete)
+void timers_resolve(emst_context* c) {
+  for (const auto& t : c->timers) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, t.a, t.b));
+    if (t.acc) *t.acc += ms;
+    if (t.trav) {
+      c->traverse_ms += ms;
+      if (c->trace) fprintf(stderr, "[emst] round %d traverse [%lld, %lld): %.3f ms\n", t.round, t.q0, t.q1, ms);
+    }
+  }
+  c->timers.clear();
+  c->ev_next = 0;
+}
+
 void read_counters(emst_context* c) {
   CK(cudaMemcpyAsync(c->host_counters, c->counters.p, kCounters * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  timers_resolve(c);
+  if (c->front_pending) {   // the labelling kernel's count of nodes still mixed
+    c->front_n = (long long)(unsigned)c->host_counters[8];
+    c->front_pending = false;
+    if (c->trace) fprintf(stderr, "[emst] comps %lld: %lld nodes still mixed\n", c->round_comps, c->front_n);
+  }
 }
 
 // ------------------------------------------------------------------- scan
@@ -427,7 +471,7 @@ void launch_labels(emst_context* c, long long n, LabelMode mode, bool want_top) 
 void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds,
                    bool want_top = false, LabelMode mode = kLabelsFull) {
   c->top_valid = false;
-  CK(cudaEventRecord(c->ev_a, c->stream));
+  cudaEvent_t e0 = timer_event(c);
   run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds, c->core}, false);
   // window seeds pay while components are small and in 3D (measured: 37M blobs 3D
   // -2.3 ms, 10M normal 3D -0.6 ms; the 2D configs lose ~1 %); later rounds gain nothing
@@ -438,28 +482,16 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
     launch(c, kern, grid_for(n, kSeedThreads), kSeedThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, W,
            c->ub.p);
   }
-  CK(cudaEventRecord(c->ev_b, c->stream));
+  cudaEvent_t e1 = timer_event(c);
   if (n > 1 && mode != kLabelsNone) {
     if (c->dim == 3) launch_labels<Node3>(c, n, mode, want_top);
     else launch_labels<Node2>(c, n, mode, want_top);
     c->top_valid = want_top && mode == kLabelsFrontier;
   }
-  cudaEvent_t ev_c;
-  CK(cudaEventCreate(&ev_c));
-  CK(cudaEventRecord(ev_c, c->stream));
-  CK(cudaEventSynchronize(ev_c));
-  float a = 0.f, b = 0.f;
-  CK(cudaEventElapsedTime(&a, c->ev_a, c->ev_b));
-  CK(cudaEventElapsedTime(&b, c->ev_b, ev_c));
-  CK(cudaEventDestroy(ev_c));
-  if (ms_bounds) *ms_bounds += a;
-  if (ms_labels) *ms_labels += b;
-  if (c->front_pending) {   // (the sync above made the count readable)
-    read_counters(c);
-    c->front_n = (long long)(unsigned)c->host_counters[8];
-    c->front_pending = false;
-    if (c->trace) fprintf(stderr, "[emst] round %d comps %lld: %lld nodes still mixed\n", c->round, c->round_comps, c->front_n);
-  }
+  cudaEvent_t e2 = timer_event(c);
+  // (no sync here: the times and the count of nodes still mixed are read at the round's counter read)
+  c->timers.push_back({e0, e1, ms_bounds, false, c->round, 0, 0});
+  c->timers.push_back({e1, e2, ms_labels, false, c->round, 0, 0});
 }
 
 template <int D, bool S, bool B, bool M, bool P, bool G = false>
@@ -479,7 +511,7 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
   // late rounds: list the queries that are not settled up front (Euclidean with bounds only)
   const bool use_list = B && !M && c->round > 1 && c->skip_frac >= c->list_skip;
   unsigned* qcount = reinterpret_cast<unsigned*>(dev_counter(c, 14));
-  CK(cudaEventRecord(c->tv_a, c->stream));
+  cudaEvent_t ta = timer_event(c);
   if (use_list) {
     c->qlist.ensure(q1 - q0);
     CK(cudaMemsetAsync(qcount, 0, sizeof(long long), c->stream));
@@ -498,13 +530,8 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
            c->top_valid ? (const int*)c->top.p : (const int*)nullptr, c->core, side,
            use_list ? (const int*)c->qlist.p : (const int*)nullptr, (const unsigned*)qcount);
   }
-  CK(cudaEventRecord(c->tv_b, c->stream));
-  CK(cudaEventSynchronize(c->tv_b));
-  float ms = 0.f;
-  CK(cudaEventElapsedTime(&ms, c->tv_a, c->tv_b));
-  c->traverse_ms += ms;
+  c->timers.push_back({ta, timer_event(c), nullptr, true, c->round, q0, q1});   // traverse_ms at the next sync
   c->traverse_launches++;
-  if (c->trace) fprintf(stderr, "[emst] round %d traverse [%lld, %lld): %.3f ms\n", c->round, q0, q1, ms);
   c->traverse_queries += q1 - q0;
 }
 
@@ -565,7 +592,9 @@ void round_find_all(emst_context* c, long long n, long long comps, int flags) {
 
 // Phase 4: collapse the successor graph; appends edges at `edge_base`, relabels.
 // Returns the new component count (and the edges emitted via *emitted).
-long long round_merge(emst_context* c, long long n, long long comps, long long edge_base, long long* emitted) {
+long long round_merge(emst_context* c, long long n, long long comps, long long edge_base, long long* emitted,
+                      double* ms_merge = nullptr) {
+  cudaEvent_t m0 = timer_event(c);
   int* err = reinterpret_cast<int*>(dev_counter(c, 2));
   launch(c, k_merge_succ, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, (const int*)c->label.p,
          (const unsigned*)c->iperm.p, c->succ.p, err);
@@ -575,7 +604,8 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
            true);
   launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->root.p, (const int*)c->newid.p, comps, c->fin.p);
   launch(c, k_relabel, grid_for(n, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
-  read_counters(c);
+  c->timers.push_back({m0, timer_event(c), ms_merge, false, c->round, 0, 0});
+  read_counters(c);   // (the round's one host sync; it also collects the round's timers)
   long long* h = c->host_counters;
   if (h[2] & kErrNoEdge) fail(EMST_ERR_NO_EDGE, "a component found no valid outgoing edge");
   if (h[2] & kErrChain) fail(EMST_ERR_CHAIN, "component chain did not terminate in a pair");
@@ -719,6 +749,8 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   CK(cudaEventCreate(&t1));
   CK(cudaEventCreate(&t2));
   CK(cudaEventCreate(&t3));
+  c->timers.clear();
+  c->ev_next = 0;
   CK(cudaEventRecord(t0, c->stream));
   build_tree(c, dev_pts, n, d);
   CK(cudaEventRecord(t3, c->stream));
@@ -760,15 +792,15 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
       const LabelMode mode = comps == n ? kLabelsNone : skip ? kLabelsFrontier : kLabelsFull;
       round_prepare(c, n, bounds, &ms_labels, &ms_bounds, skip && comps < n, mode);
     }
-    CK(cudaEventRecord(c->ev_a, c->stream));
+    cudaEvent_t f0 = timer_event(c);
     c->singleton_round = comps == n;
     round_find(c, n, comps, flags);
     c->one_side = false;
     c->singleton_round = false;
     c->round = 0;
-    CK(cudaEventRecord(c->ev_b, c->stream));
+    c->timers.push_back({f0, timer_event(c), &ms_find, false, st->iterations, 0, 0});
     long long emitted = 0;
-    long long next = round_merge(c, n, comps, edges, &emitted);
+    long long next = round_merge(c, n, comps, edges, &emitted, &ms_merge);
     if (st->iterations <= 64) {
       const int r = st->iterations - 1;
       st->round_traverse_ms[r] = c->traverse_ms - tv_before;
@@ -781,13 +813,6 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
       found_before = c->host_counters[6];
       tv_before = c->traverse_ms;
     }
-    float a = 0.f;
-    CK(cudaEventElapsedTime(&a, c->ev_a, c->ev_b));
-    ms_find += a;
-    CK(cudaEventRecord(c->ev_a, c->stream));
-    CK(cudaEventSynchronize(c->ev_a));
-    CK(cudaEventElapsedTime(&a, c->ev_b, c->ev_a));
-    ms_merge += a;
     if (c->host_counters[3]) fail(EMST_ERR_STACK, "edge traversal exceeded %d stacked nodes", kStackCapacity);
     if (next >= comps) fail(EMST_ERR_NO_REDUCE, "merge did not reduce the component count");
     edges += emitted;
@@ -893,8 +918,6 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     set_device(c);
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
-    CK(cudaEventCreate(&c->tv_a));
-    CK(cudaEventCreate(&c->tv_b));
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaMallocHost(&c->host_counters, kCounters * sizeof(long long)));
     CK(cudaEventCreate(&c->ev_a));
@@ -932,8 +955,7 @@ int emst_context_destroy(emst_context* c) {
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
-  if (c->tv_a) cudaEventDestroy(c->tv_a);
-  if (c->tv_b) cudaEventDestroy(c->tv_b);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return EMST_OK;
@@ -1029,6 +1051,8 @@ int boruvka_impl(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
     if (c) {
       c->core = nullptr;
       cudaStreamSynchronize(c->stream);
+      c->timers.clear();   // (they may point at the failed solve's locals)
+      c->ev_next = 0;
     }
     return finish(f, err, errlen);
   }
@@ -1078,6 +1102,8 @@ int emst_core_distances(emst_context* c, const float* pts, int64_t n, int32_t d,
     if (c) {
       c->core = nullptr;
       cudaStreamSynchronize(c->stream);
+      c->timers.clear();   // (they may point at the failed solve's locals)
+      c->ev_next = 0;
     }
     return finish(f, err, errlen);
   }

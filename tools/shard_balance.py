@@ -20,9 +20,9 @@ def parse(path):
         m = re.search(r"round (\d+) traverse \[(\d+), (\d+)\): ([\d.]+) ms", line)
         if m:
             per[int(m.group(1))].append(float(m.group(4)))
-        m = re.search(r"round (\d+) comps (\d+): (\d+) nodes still mixed", line)
+        m = re.search(r"comps (\d+): (\d+) nodes still mixed", line)
         if m:
-            fronts[int(m.group(1))] = (int(m.group(2)), int(m.group(3)))
+            fronts[len(fronts) + 2] = (int(m.group(1)), int(m.group(2)))   # (labels run from round 2 on)
     tot_max = tot_mean = 0.0
     for r in sorted(per):
         t = per[r]
