@@ -329,56 +329,58 @@ __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __rest
 // 256 slots, the blocks' runs in claim order -- so the traversal's warps run
 // only real searches instead of cycling through settled queries.
 template <int D>
-__global__ void __launch_bounds__(256) k_prefilter(const float4* __restrict__ spts, const int* __restrict__ label,
-                                                   const unsigned long long* __restrict__ ub,
-                                                   const float* __restrict__ nfn_lb, const int* __restrict__ top,
-                                                   const int2* __restrict__ up, const Scene* __restrict__ scene_ptr,
-                                                   long long q0, long long q1, const int* __restrict__ side,
-                                                   int* __restrict__ out, unsigned* __restrict__ out_count,
-                                                   unsigned long long* __restrict__ skipped) {
-  __shared__ unsigned s_warp[8];
+__global__ void __launch_bounds__(kScanThreads) k_prefilter(const float4* __restrict__ spts, const int* __restrict__ label,
+                                                            const unsigned long long* __restrict__ ub,
+                                                            const float* __restrict__ nfn_lb, const int* __restrict__ top,
+                                                            const int2* __restrict__ up, const Scene* __restrict__ scene_ptr,
+                                                            long long q0, long long q1, const int* __restrict__ side,
+                                                            int* __restrict__ out, unsigned* __restrict__ out_count,
+                                                            unsigned long long* __restrict__ skipped) {
+  // a thread owns kScanItems consecutive slots of a kScanTile-slot tile; one
+  // list append (atomic) per tile, the tile's kept slots in Morton order
   __shared__ unsigned s_base;
   const Scene sc = *scene_ptr;
   const int skip_comp = side ? *side : -1;
-  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
   unsigned long long nskip = 0;
-  for (long long base = q0 + (long long)blockIdx.x * 256; base < q1; base += (long long)gridDim.x * 256) {
-    const long long s = base + threadIdx.x;
-    bool keep = false;
-    if (s < q1) {
+  for (long long t0 = q0 + (long long)blockIdx.x * kScanTile; t0 < q1; t0 += (long long)gridDim.x * kScanTile) {
+    const long long i0 = t0 + (long long)threadIdx.x * kScanItems;
+    unsigned keep = 0;   // bit j: slot i0 + j is listed
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      const long long s = i0 + j;
+      if (s >= q1) break;
       const int comp = label[s];
       const double radius = bits_to_radius(__ldcg(&ub[comp]));
-      keep = !((double)nfn_lb[s] > radius) && comp != skip_comp;
-      if (keep && top) {
+      bool k = !((double)nfn_lb[s] > radius) && comp != skip_comp;
+      if (k && top) {
         const int t = top[s];
         if (t > 0) {
           const int2 ut = __ldg(up + (t - 1));
           if (ut.x < 0) {
-            keep = false;
+            k = false;
           } else if (radius < 1e300) {
             const float4 pv = spts[s];
             const float q[3] = {pv.x, pv.y, pv.z};
-            if (ut.y <= ball_prefix<D>(q, radius, sc)) keep = false;
+            if (ut.y <= ball_prefix<D>(q, radius, sc)) k = false;
           }
         }
       }
-      nskip += !keep;
+      keep |= (unsigned)k << j;
+      nskip += !k;
     }
-    const unsigned m = __ballot_sync(0xffffffffu, keep);
-    if (lane == 0) s_warp[wid] = __popc(m);
+    unsigned total;
+    const unsigned off = block_exclusive<unsigned>(__popc(keep), &total);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(out_count, total) : 0u;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned run = 0;
-      for (int w = 0; w < 8; ++w) { const unsigned c = s_warp[w]; s_warp[w] = run; run += c; }
-      s_base = run ? atomicAdd(out_count, run) : 0u;
-    }
-    __syncthreads();
-    if (keep) out[s_base + s_warp[wid] + __popc(m & ((1u << lane) - 1u))] = (int)s;
-    __syncthreads();
+    unsigned pos = s_base + off;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j)
+      if (keep >> j & 1u) out[pos++] = (int)(i0 + j);
+    __syncthreads();   // (s_base is rewritten by the next tile)
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nskip += __shfl_xor_sync(0xffffffffu, nskip, o);
-  if (lane == 0 && nskip) atomicAdd(skipped, nskip);
+  if ((threadIdx.x & 31u) == 0 && nskip) atomicAdd(skipped, nskip);
 }
 
 // slots whose label is `value` (warp-aggregated)

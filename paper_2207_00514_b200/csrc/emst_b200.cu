@@ -515,8 +515,8 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
   if (use_list) {
     c->qlist.ensure(q1 - q0);
     CK(cudaMemsetAsync(qcount, 0, sizeof(long long), c->stream));
-    const unsigned pg = (unsigned)std::min<long long>(grid_for(q1 - q0, 256), (long long)c->num_sms * 8);
-    launch(c, k_prefilter<D>, pg, 256, 0, (const float4*)c->spts.p, (const int*)c->label.p,
+    const unsigned pg = (unsigned)std::min<long long>(grid_for(q1 - q0, kScanTile), (long long)c->num_sms * 8);
+    launch(c, k_prefilter<D>, pg, kScanThreads, 0, (const float4*)c->spts.p, (const int*)c->label.p,
            (const unsigned long long*)c->ub.p, (const float*)c->nfn_lb.p,
            c->top_valid ? (const int*)c->top.p : (const int*)nullptr, (const int2*)c->up.p, (const Scene*)c->scene.p,
            q0, q1, side, c->qlist.p, qcount, reinterpret_cast<unsigned long long*>(dev_counter(c, 9)));
