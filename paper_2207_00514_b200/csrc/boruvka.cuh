@@ -277,6 +277,7 @@ __global__ void k_fill_top(const int4* __restrict__ big, const unsigned* __restr
 // `list` = the nodes mixed last round (nullptr: all m nodes); the nodes still
 // mixed are appended to out_list (warp-aggregated).
 constexpr int kInside = -2;
+constexpr int kLabelThreads = 256;   // k_node_labels_front block size (its append is per block)
 
 template <class Node>
 __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __restrict__ range,
@@ -311,14 +312,21 @@ __global__ void k_node_labels_front(Node* __restrict__ nodes, const int2* __rest
     // keeps its labels: no write, so its record's sector is not dirtied)
     if (lab.x != ref4.z || lab.y != ref4.w) *reinterpret_cast<int2*>(&nodes[i].ref.z) = lab;
   }
+  // one append per block: same-address atomics serialise at the L2 (~2-3 ns
+  // each), and per-warp appends were ~840K of them in round 2 at 37M
+  __shared__ unsigned s_off[kLabelThreads / 32];
+  __shared__ unsigned s_base;
   const unsigned keep = __ballot_sync(0xffffffffu, mixed);
-  if (keep) {
-    unsigned base = 0;
-    const unsigned lane = threadIdx.x & 31u;
-    if (lane == (unsigned)(__ffs(keep) - 1)) base = atomicAdd(out_count, (unsigned)__popc(keep));
-    base = __shfl_sync(0xffffffffu, base, __ffs(keep) - 1);
-    if (mixed) out_list[base + __popc(keep & ((1u << lane) - 1u))] = i;
+  const unsigned lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+  if (lane == 0) s_off[wid] = __popc(keep);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned run = 0;
+    for (int w = 0; w < kLabelThreads / 32; ++w) { const unsigned c = s_off[w]; s_off[w] = run; run += c; }
+    s_base = run ? atomicAdd(out_count, run) : 0u;
   }
+  __syncthreads();
+  if (mixed) out_list[s_base + s_off[wid] + __popc(keep & ((1u << lane) - 1u))] = i;
 }
 
 // Late rounds settle most queries before their first visit (nearest-foreign

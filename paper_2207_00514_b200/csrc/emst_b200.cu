@@ -458,7 +458,7 @@ void launch_labels(emst_context* c, long long n, LabelMode mode, bool want_top) 
   unsigned* out_n = reinterpret_cast<unsigned*>(dev_counter(c, 8));
   CK(cudaMemsetAsync(out_n, 0, sizeof(long long), c->stream));
   if (count > 0)
-    launch(c, k_node_labels_front<Node>, grid_for(count, 256), 256, 0, nodes, (const int2*)c->range.p,
+    launch(c, k_node_labels_front<Node>, grid_for(count, kLabelThreads), kLabelThreads, 0, nodes, (const int2*)c->range.p,
            (const int*)c->bprefix.p, (const int*)c->label.p, in, count, out, out_n,
            want_top ? c->top.p : (int*)nullptr, c->big_tops.p, big_n);
   if (want_top)
