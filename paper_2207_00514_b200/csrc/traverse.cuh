@@ -121,6 +121,9 @@ constexpr int kTraverseThreads = 256;
 #ifndef EMST_TRAV_MINB3S
 #define EMST_TRAV_MINB3S 4
 #endif
+#ifndef EMST_TRAV_MINB2S
+#define EMST_TRAV_MINB2S 4
+#endif
 #ifndef EMST_TRAV_MINB2
 #define EMST_TRAV_MINB2 4
 #endif
@@ -273,7 +276,7 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
 // kSingle: round 1 compiled on its own (every query its own component, nothing
 // is ever "same component", no shared radius).
 template <int D, bool kSkip, bool kBounds, bool kMrd, bool kProof, bool kSingle>
-__global__ void __launch_bounds__(kTraverseThreads, D == 3 ? (kSingle ? EMST_TRAV_MINB3S : EMST_TRAV_MINB3) : EMST_TRAV_MINB2)
+__global__ void __launch_bounds__(kTraverseThreads, D == 3 ? (kSingle ? EMST_TRAV_MINB3S : EMST_TRAV_MINB3) : (kSingle ? EMST_TRAV_MINB2S : EMST_TRAV_MINB2))
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
