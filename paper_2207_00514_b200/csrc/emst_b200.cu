@@ -507,9 +507,9 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
                                                                              blocks_needed));
   unsigned long long* work = reinterpret_cast<unsigned long long*>(dev_counter(c, 4));
   CK(cudaMemsetAsync(work, 0, sizeof(unsigned long long), c->stream));
-  const int* side = c->one_side ? (const int*)dev_counter(c, 13) : (const int*)nullptr;
+  const int* side = c->one_side && P ? (const int*)dev_counter(c, 13) : (const int*)nullptr;
   // late rounds: list the queries that are not settled up front (Euclidean with bounds only)
-  const bool use_list = B && !M && c->round > 1 && c->skip_frac >= c->list_skip;
+  const bool use_list = P && B && !M && c->round > 1 && c->skip_frac >= c->list_skip;
   unsigned* qcount = reinterpret_cast<unsigned*>(dev_counter(c, 14));
   cudaEvent_t ta = timer_event(c);
   if (use_list) {
@@ -566,6 +566,7 @@ void traverse_dispatch(emst_context* c, int flags, EdgeKey* out, long long q0, l
 void round_find_all(emst_context* c, long long n, long long comps, int flags);
 void round_find(emst_context* c, long long n, long long comps, int flags) {
   round_find_all(c, n, comps, flags);
+  // (only the proof kernels leave a side out; after the others the copy rewrites the same edge)
   if (c->one_side) launch(c, k_copy_key, 1, 32, 0, c->best.p, (const int*)dev_counter(c, 13));
 }
 void round_find_all(emst_context* c, long long n, long long comps, int flags) {

@@ -121,6 +121,9 @@ constexpr int kTraverseThreads = 256;
 #ifndef EMST_TRAV_MINB3S
 #define EMST_TRAV_MINB3S 4
 #endif
+#ifndef EMST_TRAV_MINB3R2
+#define EMST_TRAV_MINB3R2 4
+#endif
 #ifndef EMST_TRAV_MINB2S
 #define EMST_TRAV_MINB2S 4
 #endif
@@ -276,7 +279,7 @@ __device__ __forceinline__ bool visit_child(const Rec& rec, int side, const floa
 // kSingle: round 1 compiled on its own (every query its own component, nothing
 // is ever "same component", no shared radius).
 template <int D, bool kSkip, bool kBounds, bool kMrd, bool kProof, bool kSingle>
-__global__ void __launch_bounds__(kTraverseThreads, D == 3 ? (kSingle ? EMST_TRAV_MINB3S : EMST_TRAV_MINB3) : (kSingle ? EMST_TRAV_MINB2S : EMST_TRAV_MINB2))
+__global__ void __launch_bounds__(kTraverseThreads, D == 3 ? (kSingle ? EMST_TRAV_MINB3S : kProof ? EMST_TRAV_MINB3 : EMST_TRAV_MINB3R2) : (kSingle ? EMST_TRAV_MINB2S : EMST_TRAV_MINB2))
 k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __restrict__ spts,
            const unsigned* __restrict__ perm, const int* __restrict__ label, unsigned long long* ub,
            EdgeKey* __restrict__ best, long long q0, long long q1, const Box3* __restrict__ root_box,
@@ -287,8 +290,9 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            const int* __restrict__ qlist_in, const unsigned* __restrict__ qcount) {
   // round 1 (kSingle) has no pure nodes, no one-sided round, no query list and no earlier proofs
   const int* __restrict__ top_pure = kSingle ? nullptr : top_pure_in;
-  const int* __restrict__ side = kSingle ? nullptr : side_in;
-  const int* __restrict__ qlist = kSingle ? nullptr : qlist_in;
+  // (query lists and the one-sided last round come with the proof kernels only)
+  const int* __restrict__ side = kSingle || !kProof ? nullptr : side_in;
+  const int* __restrict__ qlist = kSingle || !kProof ? nullptr : qlist_in;
   constexpr bool kNlb = kBounds && !kSingle;
   // qlist: the slots to run (k_prefilter dropped the ones settled up front), else all of [q0, q1)
   // mutual reachability (kMrd): core distances per slot; compiled out otherwise
