@@ -604,7 +604,7 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
   run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->euv.p, c->ew.p, edge_base, c->newid.p},
            true);
   launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->root.p, (const int*)c->newid.p, comps, c->fin.p);
-  launch(c, k_relabel, grid_for(n, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
+  launch(c, k_relabel, grid_for((n + 3) / 4, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
   c->timers.push_back({m0, timer_event(c), ms_merge, false, c->round, 0, 0});
   read_counters(c);   // (the round's one host sync; it also collects the round's timers)
   long long* h = c->host_counters;
