@@ -26,7 +26,33 @@ k_scene(const float* __restrict__ pts, long long n, float* __restrict__ part_lo,
 #pragma unroll
   for (int k = 0; k < D; ++k) { lo[k] = __int_as_float(0x7f800000); hi[k] = -__int_as_float(0x7f800000); }
   long long bad = 0x7fffffffffffffffll;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // 16-byte aligned input (the usual case): 4 points per step as D float4 loads
+  const bool vec = (reinterpret_cast<unsigned long long>(pts) & 15ull) == 0;
+  const long long nv = vec ? n / 4 : 0;
+  for (long long t = t0; t < nv; t += stride) {
+    const float4* v = reinterpret_cast<const float4*>(pts) + t * D;
+    float f[4 * D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+      const float4 x = __ldg(v + j);
+      f[4 * j] = x.x; f[4 * j + 1] = x.y; f[4 * j + 2] = x.z; f[4 * j + 3] = x.w;
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      bool fin = true;
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        const float x = f[p * D + k];
+        fin &= isfinite(x);
+        lo[k] = fminf(lo[k], x);
+        hi[k] = fmaxf(hi[k], x);
+      }
+      if (!fin && 4 * t + p < bad) bad = 4 * t + p;
+    }
+  }
+  for (long long i = nv * 4 + t0; i < n; i += stride) {
     bool fin = true;
 #pragma unroll
     for (int k = 0; k < D; ++k) {
@@ -71,9 +97,10 @@ k_scene(const float* __restrict__ pts, long long n, float* __restrict__ part_lo,
     s_last = done == gridDim.x - 1;
   }
   __syncthreads();
-  if (!s_last || threadIdx.x != 0) return;
+  if (!s_last) return;
+  // the last block folds the per-block partials, all its threads at once
   __threadfence();
-  for (unsigned b = 0; b < gridDim.x; ++b) {
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
 #pragma unroll
     for (int k = 0; k < D; ++k) {
       lo[k] = fminf(lo[k], __ldcg(&part_lo[b * D + k]));
@@ -81,6 +108,29 @@ k_scene(const float* __restrict__ pts, long long n, float* __restrict__ part_lo,
     }
     long long pb = __ldcg(&part_bad[b]);
     bad = pb < bad ? pb : bad;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      lo[k] = fminf(lo[k], __shfl_xor_sync(0xffffffffu, lo[k], o));
+      hi[k] = fmaxf(hi[k], __shfl_xor_sync(0xffffffffu, hi[k], o));
+    }
+    long long bb = __shfl_xor_sync(0xffffffffu, bad, o);
+    bad = bb < bad ? bb : bad;
+  }
+  __syncthreads();   // (s_lo / s_hi / s_bad are reused)
+  if (lane_id() == 0) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) { s_lo[k][w] = lo[k]; s_hi[k][w] = hi[k]; }
+    s_bad[w] = bad;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int j = 1; j < kSceneThreads / 32; ++j) {
+#pragma unroll
+    for (int k = 0; k < D; ++k) { lo[k] = fminf(lo[k], s_lo[k][j]); hi[k] = fmaxf(hi[k], s_hi[k][j]); }
+    bad = s_bad[j] < bad ? s_bad[j] : bad;
   }
   scene->bad_row = bad;
 #pragma unroll
