@@ -143,6 +143,35 @@ struct RoundScanOp {
   }
 };
 
+// Round 1 of the solve: every slot is its own component (labels are the slot
+// ids), so the boundary-pair fold of the round scan reduces to
+// ub[s] = min(w(s-1, s), w(s, s+1)) with the same exact weights (mst.py:198-224):
+// one streaming pass, no atomics, and no boundary prefix (round 1 labels no nodes).
+template <int D>
+__global__ void k_seed_round1(const float4* __restrict__ spts, long long n, const double* __restrict__ core,
+                              unsigned long long* __restrict__ ub) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const float4 a = spts[s];
+  const float pa[3] = {a.x, a.y, a.z};
+  double w = __longlong_as_double(0x7ff0000000000000ll);
+  if (s > 0) {
+    const float4 b = spts[s - 1];
+    const float pb[3] = {b.x, b.y, b.z};
+    double d = exact_dist<D>(pb, pa);
+    if (core) d = fmax(d, fmax(core[s - 1], core[s]));
+    w = d;
+  }
+  if (s + 1 < n) {
+    const float4 b = spts[s + 1];
+    const float pb[3] = {b.x, b.y, b.z};
+    double d = exact_dist<D>(pa, pb);
+    if (core) d = fmax(d, fmax(core[s], core[s + 1]));
+    w = fmin(w, d);
+  }
+  ub[s] = s > 0 || s + 1 < n ? (unsigned long long)__double_as_longlong(w) : ~0ull;
+}
+
 // Extra radius seeds for the solve (not the reference's building block): slot
 // s pairs with its Z-order neighbours s-W .. s+W (the direct neighbours are
 // already in the boundary scan).  A pair in different components is a real

@@ -472,7 +472,15 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
                    bool want_top = false, LabelMode mode = kLabelsFull) {
   c->top_valid = false;
   cudaEvent_t e0 = timer_event(c);
-  run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds, c->core}, false);
+  if (mode == kLabelsNone && c->round == 1) {
+    // round 1 of the solve: singletons, no node labels, so no boundary prefix either
+    if (bounds) {
+      if (c->dim == 3) launch(c, k_seed_round1<3>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, c->core, c->ub.p);
+      else launch(c, k_seed_round1<2>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, c->core, c->ub.p);
+    }
+  } else {
+    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds, c->core}, false);
+  }
   // window seeds pay while components are small and in 3D (measured: 37M blobs 3D
   // -2.3 ms, 10M normal 3D -0.6 ms; the 2D configs lose ~1 %); later rounds gain nothing
   if (bounds && c->seed_window > 1 && c->dim == 3 && c->round >= c->seed_from && !c->core && c->round_comps * 1024 >= n) {
