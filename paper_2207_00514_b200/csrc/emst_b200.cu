@@ -601,12 +601,13 @@ void round_find_all(emst_context* c, long long n, long long comps, int flags) {
 
 // Phase 4: collapse the successor graph; appends edges at `edge_base`, relabels.
 // Returns the new component count (and the edges emitted via *emitted).
+// singletons: the solve's round 1, where label[s] == s
 long long round_merge(emst_context* c, long long n, long long comps, long long edge_base, long long* emitted,
-                      double* ms_merge = nullptr) {
+                      double* ms_merge = nullptr, bool singletons = false) {
   cudaEvent_t m0 = timer_event(c);
   int* err = reinterpret_cast<int*>(dev_counter(c, 2));
   launch(c, k_merge_succ, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, (const int*)c->label.p,
-         (const unsigned*)c->iperm.p, c->succ.p, err);
+         (const unsigned*)c->iperm.p, c->succ.p, err, singletons);
   launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
   launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, c->root.p, err);
   run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->euv.p, c->ew.p, edge_base, c->newid.p},
@@ -809,7 +810,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     c->round = 0;
     c->timers.push_back({f0, timer_event(c), &ms_find, false, st->iterations, 0, 0});
     long long emitted = 0;
-    long long next = round_merge(c, n, comps, edges, &emitted, &ms_merge);
+    long long next = round_merge(c, n, comps, edges, &emitted, &ms_merge, comps == n);
     if (st->iterations <= 64) {
       const int r = st->iterations - 1;
       st->round_traverse_ms[r] = c->traverse_ms - tv_before;
