@@ -13,3 +13,5 @@ for cfg in blobs2d_24m uniform2d_10m normal3d_10m; do
 done
 bash tools/ncu_profiles.sh
 CFG=blobs2d_24m bash tools/ncu_step.sh
+# mutual reachability at the headline size (k_pts 4 and 16)
+for k in 4 16; do PYTHONPATH=$PWD timeout 300 python tools/mrd_timing.py blobs3d_37m $k > gpurun_out/mrd_k$k.log 2>&1; done
