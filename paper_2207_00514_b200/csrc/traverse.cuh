@@ -112,23 +112,30 @@ __device__ __forceinline__ unsigned lanemask_lt_u32() {
   return m;
 }
 
-constexpr int kTraverseThreads = 256;
-// resident blocks per SM: 3D lanes use the extra registers (85) better, 2D
-// lanes prefer the extra warps (measured: 3D 3 blocks -1.5 %, 2D 4 blocks -17 %)
+#ifndef EMST_TRAV_THREADS
+#define EMST_TRAV_THREADS 128
+#endif
+constexpr int kTraverseThreads = EMST_TRAV_THREADS;
+// Resident 128-thread blocks per SM.  The 3D proof kernels (rounds >= 3) need
+// their registers: 7 blocks = 72 registers, no spill, 28 warps (256-thread
+// blocks could only pick 80 registers / 24 warps or 64 with 102 B of spills:
+// 37M blobs 3D -1.3 ms for 128 x 7).  Every other variant fits 64 registers
+// (8 blocks, 32 warps); 2D lanes prefer the extra warps (-17 % vs 48 warps less).
+// Round 1 (kSingle) and the 3D round-2 kernel (no proof) have their own knobs.
 #ifndef EMST_TRAV_MINB3
-#define EMST_TRAV_MINB3 3
+#define EMST_TRAV_MINB3 7
 #endif
 #ifndef EMST_TRAV_MINB3S
-#define EMST_TRAV_MINB3S 4
+#define EMST_TRAV_MINB3S 8
 #endif
 #ifndef EMST_TRAV_MINB3R2
-#define EMST_TRAV_MINB3R2 4
+#define EMST_TRAV_MINB3R2 8
 #endif
 #ifndef EMST_TRAV_MINB2S
-#define EMST_TRAV_MINB2S 4
+#define EMST_TRAV_MINB2S 8
 #endif
 #ifndef EMST_TRAV_MINB2
-#define EMST_TRAV_MINB2 4
+#define EMST_TRAV_MINB2 8
 #endif
 #ifndef EMST_REFILL_IDLE
 #define EMST_REFILL_IDLE 16
