@@ -132,7 +132,7 @@ constexpr int kTraverseThreads = EMST_TRAV_THREADS;
 #define EMST_TRAV_MINB3R2 7
 #endif
 #ifndef EMST_TRAV_MINB2S
-#define EMST_TRAV_MINB2S 8
+#define EMST_TRAV_MINB2S 9
 #endif
 #ifndef EMST_TRAV_MINB2
 #define EMST_TRAV_MINB2 8
