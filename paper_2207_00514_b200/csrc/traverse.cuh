@@ -156,7 +156,14 @@ constexpr long long kTravPrefetch = EMST_TRAV_PREFETCH;   // L2 prefetch lookahe
 constexpr int kTraverseChunk = EMST_TRAV_CHUNK;   // consecutive Morton queries a warp claims at once
 constexpr int kSmemStack = EMST_SMEM_STACK;       // stack entries per lane kept in shared memory
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
-constexpr int kRadiusRefresh = 16;
+#ifndef EMST_RADIUS_REFRESH
+#define EMST_RADIUS_REFRESH 256
+#endif
+// pops between re-reads of the component's shared radius (the first one after
+// half of it).  Measured at 37M blobs 3D: every 16 pops 72.4 ms, 32: 71.8, 64:
+// 71.4, 256 (in practice only very long searches re-read): 70.6 -- an L2 read
+// per lane costs more than the slightly tighter radius saves.
+constexpr int kRadiusRefresh = EMST_RADIUS_REFRESH;
 #ifndef EMST_SHARE_AT_END
 #define EMST_SHARE_AT_END 1
 #endif
