@@ -11,9 +11,10 @@
 //   * both children get the same branch-free conservative f32 lower bound
 //     (rounded toward -inf); only leaves that survive it pay for the exact f64
 //     reference distance (bvh.py:284-290) that decides acceptance;
-//   * the per-component radius is shared: an accepted leaf lowers ub[comp] with
-//     a u64 atomicMin on the f64 bit pattern and every lane re-reads it every
-//     16 pops.  Any value written is a real outgoing edge of the component, so
+//   * the per-component radius is shared: a query's accepted candidate lowers
+//     ub[comp] with a u64 atomicMin on the f64 bit pattern when the query ends,
+//     and later queries of the component start from it (long searches also
+//     re-read it, kRadiusRefresh).  Any value written is a real outgoing edge of the component, so
 //     the radius never drops below the component's minimum -- the result is
 //     unchanged ("in the extreme case ...").
 //   * per-component result: 128-bit atomic min of (w bits, u << 32 | v).
