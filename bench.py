@@ -3,16 +3,18 @@
 
 One "step" is one full ``boruvka_emst`` of the synthetic cloud (build + all
 Boruvka rounds + final (w, u, v) edge sort), points resident in HBM before the
-timed region (``value``) or copied from pinned host memory with the edges read
-back inside it (``e2e``, through the public drop-in API).
+timed region (``value``) or handed over as a plain numpy array with the edges
+read back inside it (``e2e``, through the public drop-in API).  The output of
+the timed run is digested and compared with the reference's (``parity``).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config blobs3d_37m] [--impl ours|reference]
 
-N > 1 runs under torchrun, one process per GPU: every rank builds the same tree
-and takes a Morton slot range of each round's traversal; per-component minima
-meet in a two-phase NCCL min-allreduce (strong scaling: total work fixed).
+N > 1 runs one process per GPU (under torchrun; without it bench.py relaunches
+itself through torchrun): every rank builds the same tree and takes a Morton
+slot range of each round's traversal; per-component minima meet in a
+two-phase NCCL min-allreduce (strong scaling: total work fixed).
 ``--impl reference`` times the reference algorithm's CPU implementation (the C
-restatement in oracle/, all host threads) on a bounded sample of the same cloud.
+restatement in oracle/, all host threads) on the same whole cloud.
 """
 
 from __future__ import annotations
@@ -133,42 +135,108 @@ def cpu_sample(points, m: int):
     return E.sample(points, min(m, points.shape[0]), 0)
 
 
-def time_oracle(points, m: int):
-    """Reference CPU algorithm (oracle/ C restatement, OpenMP on all host threads) on an m-point sample."""
-    from oracle import oracle as orc
-    sub = cpu_sample(points, m)
-    orc.set_threads(os.cpu_count() or 1)
-    t0 = time.perf_counter()
-    orc.boruvka_emst(sub)
-    dt = time.perf_counter() - t0
-    return sub.shape[0] * sub.shape[1] / dt / 1e6, dt, orc.num_threads(), sub.shape[0]
-
-
 def run_reference(args):
+    """The reference arm: the reference algorithm's CPU implementation on the headline cloud itself.
+
+    Every timed step is one full solve of the whole config (same n, d, seed as our arm, so the
+    driver's ratio compares like with like).  The C restatement runs on all host threads; it needs
+    no JIT, so the W warm-up steps touch the code and memory on a 1M-point sample instead of
+    repeating full 37M solves.  Timed steps stop early (reported as `steps_timed`) if they would run
+    past --ref-budget seconds.
+    """
     world, rank, _ = dist_env()
     cfg = args.config
     kind, n, d, seed = CONFIGS[cfg]
     if rank != 0:
         return
+    from oracle import oracle as orc
     pts = make_points(cfg)
-    m = args.cpu_sample
-    rates = []
-    for i in range(args.warmup + args.steps):
-        rate, dt, threads, msz = time_oracle(pts, m)
-        if i >= args.warmup:
-            rates.append((rate, dt))
-    value = statistics.median(r for r, _ in rates)
-    ms = statistics.median(t for _, t in rates) * 1e3
-    sample = f"{m}-point uniform subsample (reference data.sample, seed 0) of the {cfg} cloud per step"
+    orc.set_threads(os.cpu_count() or 1)
+    threads = orc.num_threads()
+    warm = cpu_sample(pts, min(1_000_000, n))
+    for _ in range(args.warmup):
+        orc.boruvka_emst(warm)
+    times = []
+    t_begin = time.perf_counter()
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        res = orc.boruvka_emst(pts)
+        times.append(time.perf_counter() - t0)
+        spent = time.perf_counter() - t_begin
+        if spent + statistics.median(times) > args.ref_budget and i + 1 < args.steps:
+            break
+    dt = statistics.median(times)
+    value = n * d / dt / 1e6
+    sample = f"the whole {cfg} cloud (n={n}) per step, {threads} OpenMP threads"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "MFeatures/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32 coords / f64 weights", "data": "synthetic",
-        "config": {"workload": cfg, "kind": kind, "n": n, "d": d, "seed": seed, "sample_points": m},
+        "steps": args.steps, "steps_timed": len(times), "warmup": args.warmup, "ms_per_step": dt * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32 coords / f64 weights",
+        "data": "synthetic (reference generator, seed 0)",
+        "config": {"workload": cfg, "kind": kind, "n": n, "d": d, "seed": seed,
+                   "warmup_sample_points": warm.shape[0]},
         "cpu_baseline": {"value": value, "unit": "MFeatures/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "MFeatures/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "parity": parity_record(cfg, res.edges, res.weights),
     }
     print(json.dumps(line), flush=True)
+
+
+def parity_record(cfg: str, edges, weights) -> dict:
+    """sha256(edges || weights)[:16] of a run's output against the reference's own (tests/golden/large.json)."""
+    import hashlib
+    e = np.ascontiguousarray(edges, dtype="<i8")
+    w = np.ascontiguousarray(weights, dtype="<f8")
+    got = hashlib.sha256(e.tobytes() + w.tobytes()).hexdigest()[:16]
+    want = None
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "large.json")) as fh:
+            want = json.load(fh)[cfg]["digest"]
+    except Exception:
+        pass
+    return {"digest": got, "reference_digest": want, "ok": want is not None and got == want}
+
+
+def setup_ranks(world: int, rank: int, local: int):
+    """(context, torch.distributed module or None, description) for this rank.
+
+    One process per GPU over NCCL when there are enough GPUs; with fewer GPUs than
+    ranks (a single-GPU box) the ranks share devices and exchange through the host
+    (gloo) -- the same sharded traversal and exchange kernels, another transport.
+    """
+    import torch
+    import paper_2207_00514_b200 as E
+    from paper_2207_00514_b200 import distributed as D
+
+    if world == 1:
+        torch.cuda.set_device(local)
+        return E.Context(local), None, {"devices": 1, "exchange": "none"}
+    import torch.distributed as dist
+    ndev = torch.cuda.device_count()
+    if ndev >= world:
+        device = local
+        torch.cuda.set_device(device)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+        exchange = "nccl"
+    else:
+        device = local % ndev
+        torch.cuda.set_device(device)
+        dist.init_process_group("gloo")
+        exchange = "host"
+    ctx = D.init_context(device=device, exchange=exchange)
+    desc = {"devices": min(ndev, world), "exchange": exchange}
+    if exchange == "host":
+        desc["note"] = f"{world} ranks share {ndev} GPU(s): host (gloo) exchange; not a scaling measurement"
+    return ctx, dist, desc
+
+
+def max_over_ranks(dist, x: float) -> float:
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], device="cuda" if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def run_ours(args):
@@ -178,16 +246,7 @@ def run_ours(args):
     world, rank, local = dist_env()
     cfg = args.config
     kind, n, d, seed = CONFIGS[cfg]
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        obj = [E.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        ctx = E.Context(local, rank, world, obj[0])
-    else:
-        ctx = E.Context(local)
+    ctx, dist, ranks = setup_ranks(world, rank, local)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream)
 
@@ -211,7 +270,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     trav_ms = trav_launch = launches = 0
-    with ClockSampler(local) as clocks:
+    with ClockSampler(torch.cuda.current_device()) as clocks:
         start.record(stream)
         for _ in range(args.steps):
             st = step()
@@ -222,33 +281,28 @@ def run_ours(args):
         torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    ms = start.elapsed_time(end) / args.steps
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(dist, start.elapsed_time(end) / args.steps)
     value = n * d / (ms / 1e3) / 1e6
     counts = [int(st.component_counts[i]) for i in range(st.num_counts)]
+    # parity of the exact run just timed: the last step's device-resident output against the reference
+    parity = parity_record(cfg, edges.cpu().numpy(), weights.cpu().numpy())
+    del pts_dev
 
-    # end to end through the public drop-in: pinned host points in, host edges/weights out
-    pinned = torch.from_numpy(pts_host).pin_memory()
-    host_view = pinned.numpy()
+    # end to end through the public drop-in as a caller uses it: a plain (pageable) numpy array in,
+    # numpy edges / weights out, every copy inside the timed region
     e2e_ms = []
     for i in range(max(2, min(args.steps, 3)) + 1):
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = E.boruvka_emst(host_view, context=ctx)
+        res = E.boruvka_emst(pts_host, context=ctx)
         dt = (time.perf_counter() - t0) * 1e3
         if i > 0:
             e2e_ms.append(dt)
-    e2e = statistics.median(e2e_ms)
-    if dist is not None:
-        t = torch.tensor([e2e], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e = float(t.item())
+    e2e = max_over_ranks(dist, statistics.median(e2e_ms))
     assert res.component_counts == counts
+    e2e_parity = parity_record(cfg, res.edges, res.weights)
 
     peak, peak_src = hbm_peak()
     # dominant kernel: the traversal; algorithmic bytes per query per round = 12d + 36
@@ -265,15 +319,17 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 coords / f64 weights", "data": "synthetic (reference generator, seed 0)",
         "config": {"workload": cfg, "kind": kind, "n": n, "d": d, "seed": seed,
-                   "parallelism": f"replicated tree, traversal sharded by Morton range x{world}",
+                   "parallelism": f"replicated tree, traversal sharded by Morton range x{world}", **ranks,
                    "l2": "inputs larger than L2 (points 444 MB + 2.4 GB tree at 37M), no flush"},
+        "parity": parity,
         "e2e": {"value": n * d / (e2e / 1e3) / 1e6, "unit": "MFeatures/s", "ms_per_step": e2e,
+                "input": "pageable numpy array through boruvka_emst", "parity_ok": e2e_parity["ok"],
                 "h2d_bytes_per_step": n * d * 4, "d2h_bytes_per_step": (n - 1) * 24},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "kernel": "k_traverse", "achieved": trav_gbs, "peak": peak, "unit": "GB/s",
                      "frac": trav_gbs / peak, "traffic": measured_traffic(cfg),
                      "traffic_source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per k_traverse launch "
-                                       "(profiles/r01_traverse_traffic.json)",
+                                       f"({os.path.relpath(TRAFFIC_PATH, ROOT)})",
                      "algorithmic_bytes_per_launch": trav_bytes / max(st.traverse_launches, 1),
                      "peak_source": peak_src,
                      "bytes_model": f"(12d+36) B per query per round = {12 * d + 36} B",
@@ -287,12 +343,31 @@ def run_ours(args):
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        rate, dt, threads, msz = time_oracle(pts_host, args.cpu_sample * 2)
-        line["cpu_baseline"] = {"value": rate, "unit": "MFeatures/s", "cores": threads, "kind": "port",
-                                "sample": f"{msz}-point subsample (data.sample seed 0) of {cfg}, {dt:.1f} s"}
+        from oracle import oracle as orc
+        orc.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        orc.boruvka_emst(pts_host)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": n * d / dt / 1e6, "unit": "MFeatures/s", "cores": orc.num_threads(),
+                                "kind": "port", "sample": f"the whole {cfg} cloud (n={n}), one solve, {dt:.1f} s"}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: relaunch this script as N ranks (torchrun, 127.0.0.1)."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")   # (stderr: lets the driver see the N ranks come up)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -302,10 +377,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="blobs3d_37m", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
+    ap.add_argument("--ref-budget", type=float, default=1200.0,
+                    help="reference arm: stop timing full solves after about this many seconds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="one untimed step only (for ncu); prints nothing")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -91,7 +91,8 @@ int emst_nccl_unique_id(void* id_out_128, char* err, size_t errlen);
 
 /* One context per (process, device).  world > 1 shares every Boruvka round's
  * traversal by Morton slot range over `world` ranks (replicated tree, one
- * two-phase NCCL min-reduction per round); nccl_id may be NULL when world == 1. */
+ * two-phase min-reduction per round over NCCL); nccl_id may be NULL when
+ * world == 1, or when a host exchange is set (emst_context_set_exchange). */
 int emst_context_create(int device, int rank, int world, const void* nccl_id, emst_context** out,
                         char* err, size_t errlen);
 int emst_context_destroy(emst_context* ctx);
@@ -100,10 +101,28 @@ int emst_context_destroy(emst_context* ctx);
  * the context's own stream) -- lets a caller time calls with its own events. */
 int emst_context_set_stream(emst_context* ctx, void* stream);
 
-/* Single-GPU shard emulation: split each round's traversal into `shards` Morton
- * ranges and combine them with the same two-phase min protocol the NCCL path
- * uses (for determinism tests of the multi-GPU protocol on one device). */
+/* Shards per rank: each rank's part of a round's traversal is split into `shards`
+ * Morton ranges (S = world * shards in all) whose per-component keys go through
+ * the same two-phase exchange kernels and all-reduce as N ranks do: the local
+ * rows are folded on the device, then ncclAllReduce runs on the communicator
+ * (a 1-rank communicator is created for world == 1, so one GPU exercises the
+ * whole N-rank path).  Determinism tests of the multi-GPU protocol use it. */
 int emst_context_set_virtual_shards(emst_context* ctx, int shards);
+
+/* Host exchange for ranks without an NCCL communicator (a context created with
+ * world > 1 and nccl_id == NULL): `fn` all-reduces `count` u64 in place in
+ * page-locked host memory over every rank, by unsigned min (EMST_EXCHANGE_MIN)
+ * or sum (EMST_EXCHANGE_SUM), and returns 0 on success.  The Python layer binds
+ * it to torch.distributed.all_reduce of any backend (gloo); it replaces
+ * ncclAllReduce in the two-phase exchange of mst.py:236-348's sharded query loop. */
+enum { EMST_EXCHANGE_MIN = 0, EMST_EXCHANGE_SUM = 1 };
+typedef int (*emst_exchange_fn)(uint64_t* buf, int64_t count, int32_t op, void* user);
+int emst_context_set_exchange(emst_context* ctx, emst_exchange_fn fn, void* user);
+
+/* Make the context's stream wait for the work queued so far on `stream` (a
+ * cudaStream_t, e.g. torch's current stream) -- call it before handing the
+ * library device memory that another stream produced. */
+int emst_context_wait_stream(emst_context* ctx, void* stream);
 
 /* boruvka_emst(points, "euclidean", 1, subtree_skip, upper_bound_seeding)
  * (mst.py:578-769).  edges_out: (n-1) x 2 int64, u < v; weights_out: (n-1)
@@ -132,15 +151,26 @@ void emst_text_free(void);
 int emst_core_distances(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t k_pts,
                         double* core_out, char* err, size_t errlen);
 
-/* morton_codes(points) with the tight scene bounds (geometry.py:209-227). codes_out: n u64 (host). */
+/* morton_codes(points, bounds) (geometry.py:209-227). codes_out: n u64 (host).  bounds_lo / bounds_hi:
+ * d f64 each (an Aabb; points outside are clamped into it), or both NULL for the tight scene box. */
 int emst_morton_codes(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags,
-                      uint64_t* codes_out, char* err, size_t errlen);
+                      const double* bounds_lo, const double* bounds_hi, uint64_t* codes_out, char* err,
+                      size_t errlen);
+
+/* sort_by_morton(points, bounds) (geometry.py:247-254): the stable (code, index) order, perm_out n int64
+ * (host); bounds as emst_morton_codes.  The GPU onesweep sort of the solve. */
+int emst_sort_by_morton(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags,
+                        const double* bounds_lo, const double* bounds_hi, int64_t* perm_out, char* err,
+                        size_t errlen);
 
 /* build(points) (bvh.py:305-340) in the reference's array layout (bvh.py:39-75):
- * perm n, left/right/parent n-1, leaf_parent n (int64); box_lo/box_hi (n-1) x d f32. Host outputs. */
+ * perm n, left/right/parent n-1, leaf_parent n (int64); box_lo/box_hi (n-1) x d f32. Host outputs.
+ * sweep_order (n-1) and sweep_starts (capacity n) receive the level schedule (bvh.py:293-302),
+ * *n_starts its length (height + 1); pass three NULLs to skip it. */
 int emst_build(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t* perm,
                int64_t* left, int64_t* right, int64_t* parent, int64_t* leaf_parent, float* box_lo,
-               float* box_hi, char* err, size_t errlen);
+               float* box_hi, int64_t* sweep_order, int64_t* sweep_starts, int64_t* n_starts, char* err,
+               size_t errlen);
 
 /* reduce_labels(build(points), state) (mst.py:436-448): labels n int64 (point order) -> internal labels n-1. */
 int emst_reduce_labels(emst_context* ctx, const float* pts, int64_t n, int32_t d, const int64_t* labels,

@@ -86,6 +86,8 @@ EXPORTS = (
     "emst_context_destroy",
     "emst_context_set_stream",
     "emst_context_set_virtual_shards",
+    "emst_context_set_exchange",
+    "emst_context_wait_stream",
     "emst_boruvka",
     "emst_boruvka_mrd",
     "emst_core_distances",
@@ -100,6 +102,10 @@ EXPORTS = (
     "emst_text_free",
     "emst_build_info",
 )
+
+# int (*)(uint64_t* buf, int64_t count, int32_t op, void* user): in-place all-reduce over the ranks
+EXCHANGE_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p)
+EXCHANGE_MIN, EXCHANGE_SUM = 0, 1
 
 _lib = None
 _lock = threading.Lock()
@@ -133,6 +139,8 @@ def load():
         L.emst_context_destroy.argtypes = [vp]
         L.emst_context_set_virtual_shards.argtypes = [vp, ctypes.c_int]
         L.emst_context_set_stream.argtypes = [vp, vp]
+        L.emst_context_set_exchange.argtypes = [vp, EXCHANGE_FN, vp]
+        L.emst_context_wait_stream.argtypes = [vp, vp]
         L.emst_boruvka.argtypes = [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(Stats), cp, sz]
         L.emst_boruvka_mrd.argtypes = [vp, vp, i64, i32, i32, i64, vp, vp, vp, ctypes.POINTER(Stats), cp, sz]
         L.emst_core_distances.argtypes = [vp, vp, i64, i32, i32, i64, vp, cp, sz]
@@ -185,8 +193,45 @@ class Context:
 
     def set_virtual_shards(self, shards: int) -> None:
         rc = load().emst_context_set_virtual_shards(self.handle, int(shards))
+        if rc == 11:
+            raise DeviceError("cannot create the 1-rank NCCL communicator for virtual shards")
         if rc:
             raise InvalidParameterError(f"virtual shard count {shards} out of range [1, 64]")
+
+    def set_exchange(self, allreduce) -> None:
+        """Host exchange for a world > 1 context made without an NCCL id.
+
+        ``allreduce(buf, op)`` gets a numpy uint64 view of page-locked host
+        memory and must all-reduce it in place over every rank: unsigned min
+        for ``op == EXCHANGE_MIN``, sum for ``EXCHANGE_SUM``.
+        """
+        def _cb(buf, count, op, user):
+            try:
+                arr = np.ctypeslib.as_array((ctypes.c_uint64 * int(count)).from_address(buf)) if count else \
+                    np.empty(0, np.uint64)
+                allreduce(arr, int(op))
+                return 0
+            except Exception as exc:   # (an exception cannot cross the C frame)
+                self.exchange_error = exc
+                return 1
+        self._exchange_cb = EXCHANGE_FN(_cb)   # keep the thunk alive with the context
+        self.exchange_error = None
+        raise_for(load().emst_context_set_exchange(self.handle, self._exchange_cb, None), None)
+
+    def wait_stream(self, stream) -> None:
+        """Order this context's stream after the work queued on ``stream`` (torch.cuda.Stream or raw handle)."""
+        handle = getattr(stream, "cuda_stream", stream)
+        rc = load().emst_context_wait_stream(self.handle, ctypes.c_void_p(handle) if handle else None)
+        if rc:
+            raise DeviceError(f"cudaStreamWaitEvent failed (status {rc})")
+
+    def after_torch(self, tensor) -> None:
+        """Before handing the library a CUDA tensor: wait for torch's current stream on its device, which
+        may still be producing it (the context runs on its own non-blocking stream)."""
+        import torch
+        if tensor.device.index != self.device:
+            raise InvalidParameterError(f"tensor on cuda:{tensor.device.index} given to a cuda:{self.device} context")
+        self.wait_stream(torch.cuda.current_stream(tensor.device))
 
     def set_stream(self, stream) -> None:
         """Run on an external CUDA stream (a torch.cuda.Stream or a raw cudaStream_t int; None = own)."""

@@ -93,11 +93,35 @@ def _device_points(points):
     return pts.ctypes.data, n, d, 0, pts
 
 
+def _is_cuda_tensor(x) -> bool:
+    try:
+        import torch
+    except ImportError:
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def context_for(keep, context=None) -> _lib.Context:
+    """The native context a call runs on, ordered after the stream that produced `keep`.
+
+    A CUDA tensor goes to a context on its own device (the default one for that
+    device unless `context` is given, which must then be on the same device), and
+    the context's stream first waits for torch's current stream there: the
+    tensor (or the float32 / contiguous copy _device_points made of it) may
+    still be in flight.  Host input uses the current device's default context.
+    """
+    if _is_cuda_tensor(keep):
+        ctx = context if context is not None else _lib.default_context(keep.device.index)
+        ctx.after_torch(keep)
+        return ctx
+    return context if context is not None else _lib.default_context()
+
+
 def morton_codes(points) -> np.ndarray:
     """Morton codes with the tight scene bounds, computed on the GPU (geometry.py:209-227)."""
     p, n, d, flags, keep = _device_points(points)
     out = np.empty(n, np.uint64)
-    ctx = _lib.default_context()
+    ctx = context_for(keep)
     e = _lib.err_buf()
     with ctx.lock:
         rc = _lib.load().emst_morton_codes(ctx.handle, p, n, d, flags, out.ctypes.data, e, len(e))
@@ -116,7 +140,7 @@ def build(points) -> Bvh:
     leaf_parent = np.empty(n, np.int64)
     box_lo = np.empty((max(m, 1), d), np.float32)
     box_hi = np.empty((max(m, 1), d), np.float32)
-    ctx = _lib.default_context()
+    ctx = context_for(keep)
     e = _lib.err_buf()
     with ctx.lock:
         rc = _lib.load().emst_build(ctx.handle, p, n, d, flags, perm.ctypes.data, left.ctypes.data, right.ctypes.data,

@@ -581,22 +581,17 @@ __global__ void k_join_keys(EdgeKey* __restrict__ best, const unsigned long long
   e.uv = uvmin[k];
   best[k] = e;
 }
-// In-process stand-in for the two NCCL min-allreduces over V virtual shards
-// (same two-phase protocol; used by the single-GPU shard-determinism tests).
-__global__ void k_virtual_reduce(const EdgeKey* __restrict__ shard_keys, int shards, long long c, EdgeKey* __restrict__ best) {
+// Folds rows 1..rows-1 of `buf` (row stride `stride`) into row 0 by min or sum:
+// the local (virtual-shard) stage of the exchange's all-reduce.
+__global__ void k_fold_rows(unsigned long long* __restrict__ buf, int rows, long long stride, long long c, bool sum) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= c) return;
-  unsigned long long w = ~0ull;
-  for (int g = 0; g < shards; ++g) w = min(w, shard_keys[g * c + k].w);
-  unsigned long long uv = ~0ull;
-  for (int g = 0; g < shards; ++g) {
-    EdgeKey e = shard_keys[g * c + k];
-    if (e.w == w) uv = min(uv, e.uv);
+  unsigned long long a = buf[k];
+  for (int g = 1; g < rows; ++g) {
+    const unsigned long long b = buf[g * stride + k];
+    a = sum ? a + b : min(a, b);
   }
-  EdgeKey r;
-  r.w = w;
-  r.uv = uv;
-  best[k] = r;
+  buf[k] = a;
 }
 
 // ------------------------------------------------------------ final output

@@ -390,6 +390,49 @@ k_refit(const float4* __restrict__ spts, long long n, Node* nodes, const int2* _
   }
 }
 
+// Node heights (leaf 0, internal 1 + the higher child) by the same arrival climb
+// as the refit: the second thread to reach a node knows both subtrees are done.
+// Feeds the export of the reference's level schedule (bvh.py:204-238, 293-302);
+// the solve itself never needs it.
+__global__ void k_node_heights(const int* __restrict__ leaf_parent, const int* __restrict__ node_parent, long long n,
+                               unsigned* __restrict__ arrivals, unsigned* __restrict__ height) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= n || n < 2) return;
+  unsigned h = 0;
+  int link = leaf_parent[s];
+  for (;;) {
+    const int node = link >> 1;
+    atomicMax(&height[node], h + 1);
+    unsigned prev;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&arrivals[node]) : "memory");
+    if (prev == 0 || node == 0) return;
+    h = atomicOr(&height[node], 0u);
+    link = node_parent[node];
+  }
+}
+
+__global__ void k_u32_to_u64(const unsigned* __restrict__ a, long long n, unsigned long long* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i];
+}
+
+__global__ void k_u32_to_i64(const unsigned* __restrict__ a, long long n, long long* __restrict__ out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[i];
+}
+
+// starts[k] = first position of height k + 1 in the ascending heights (np.searchsorted, left), and
+// starts[hmax] = m (bvh.py:293-302).  Heights start at 1, so starts[0] = 0.
+__global__ void k_level_starts(const unsigned long long* __restrict__ hs, const unsigned* __restrict__ order, long long m,
+                               long long* __restrict__ starts, long long* __restrict__ order_out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  order_out[i] = order[i];
+  const unsigned long long h = hs[i], hp = i > 0 ? hs[i - 1] : 0;
+  for (unsigned long long j = hp + 1; j <= h; ++j) starts[j - 1] = i;
+  if (i == m - 1) starts[h] = m;
+}
+
 // Reference-layout export of the tree (bvh.py:39-75) for parity tests.
 template <class Node>
 __global__ void k_export_tree(const Node* __restrict__ nodes, const int* __restrict__ node_parent,

@@ -55,6 +55,25 @@ struct Failure {
   } while (0)
 
 template <class T>
+struct HostBuf {   // page-locked host staging
+  T* p = nullptr;
+  size_t cap = 0;
+  void ensure_host(size_t count) {
+    if (count <= cap) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    CK(cudaMallocHost(&p, std::max<size_t>(count, 1) * sizeof(T)));
+    cap = count;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+template <class T>
 struct DevBuf {
   T* p = nullptr;
   size_t cap = 0;
@@ -100,6 +119,9 @@ struct emst_context {
   bool trace = false;             // per-round trace on stderr (EMST_TRACE=1; developer aid)
   int proof_from = 3;             // first round whose traversal records the full nearest-foreign proof (EMST_PROOF_FROM)
   ncclComm_t comm = nullptr;
+  emst_exchange_fn exch_fn = nullptr;   // host exchange (world > 1 without NCCL)
+  void* exch_user = nullptr;
+  HostBuf<unsigned long long> exch_host;
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
   long long launches = 0;
@@ -421,10 +443,6 @@ void ensure_rounds(emst_context* c, long long n) {
   c->fin.ensure(n);
   c->euv.ensure(n);
   c->ew.ensure(n);
-  if (c->world > 1) {
-    c->xw.ensure(n);
-    c->xuv.ensure(n);
-  }
 }
 
 __global__ void k_iota_int(int* a, long long n) {
@@ -577,26 +595,64 @@ void round_find(emst_context* c, long long n, long long comps, int flags) {
   // (only the proof kernels leave a side out; after the others the copy rewrites the same edge)
   if (c->one_side) launch(c, k_copy_key, 1, 32, 0, c->best.p, (const int*)dev_counter(c, 13));
 }
+// All-reduce-min (or sum) of `count` u64 over the local virtual shards (rows
+// 0..rows-1 of `buf`, `stride` apart) and then over the ranks, result in row 0.
+// The rank step is ncclAllReduce on the context's communicator (a 1-rank one
+// under virtual shards, so the NCCL call path runs on a single GPU too), or
+// the caller's host exchange callback (any torch.distributed backend).
+void allreduce_u64(emst_context* c, unsigned long long* buf, long long count, int rows, long long stride, bool sum) {
+  if (count <= 0) return;
+  if (rows > 1)
+    launch(c, k_fold_rows, grid_for(count, 256), 256, 0, buf, rows, stride, count, sum);
+  if (c->comm) {
+    NK(ncclAllReduce(buf, buf, count, ncclUint64, sum ? ncclSum : ncclMin, c->comm, c->stream));
+  } else if (c->world > 1) {
+    if (!c->exch_fn) fail(EMST_ERR_PARAM, "world %d context has neither an NCCL communicator nor an exchange", c->world);
+    c->exch_host.ensure_host(count);
+    CK(cudaMemcpyAsync(c->exch_host.p, buf, count * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->exch_fn(reinterpret_cast<uint64_t*>(c->exch_host.p), count, sum ? EMST_EXCHANGE_SUM : EMST_EXCHANGE_MIN,
+                   c->exch_user) != 0)
+      fail(EMST_ERR_NCCL, "host exchange callback failed");
+    CK(cudaMemcpyAsync(buf, c->exch_host.p, count * sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
+  }
+}
+
+// Per-component minimum over all shards of the round's queries.  A shard is
+// one Morton slot range [g n / S, (g + 1) n / S) of S = world * vshards; this
+// rank runs its vshards ranges.  With S > 1 the keys meet in the two-phase
+// exchange: min of the weight bits, then min of (u << 32 | v)
+// over the shards whose weight equals it -- exact for the 128-bit (w, u, v)
+// order, which no single u64 reduction is.
 void round_find_all(emst_context* c, long long n, long long comps, int flags) {
-  if (c->vshards > 1) {
-    const int V = c->vshards;
-    c->shard_keys.ensure((size_t)V * comps);
-    CK(cudaMemsetAsync(c->shard_keys.p, 0xff, (size_t)V * comps * sizeof(EdgeKey), c->stream));
-    for (int g = 0; g < V; ++g) traverse_dispatch(c, flags, c->shard_keys.p + (size_t)g * comps, g * n / V, (g + 1) * n / V);
-    launch(c, k_virtual_reduce, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->shard_keys.p, V, comps, c->best.p);
+  const int V = c->vshards;
+  const long long S = (long long)c->world * V;
+  if (S == 1) {
+    traverse_dispatch(c, flags, c->best.p, 0, n);
     return;
   }
-  const long long q0 = c->rank * n / c->world, q1 = (c->rank + 1) * n / c->world;
-  traverse_dispatch(c, flags, c->best.p, q0, q1);
-  if (c->world > 1) {
-    launch(c, k_split_keys, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, c->xw.p);
-    NK(ncclAllReduce(c->xw.p, c->xw.p, comps, ncclUint64, ncclMin, c->comm, c->stream));
-    launch(c, k_mask_uv, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, (const unsigned long long*)c->xw.p,
-           comps, c->xuv.p);
-    NK(ncclAllReduce(c->xuv.p, c->xuv.p, comps, ncclUint64, ncclMin, c->comm, c->stream));
-    launch(c, k_join_keys, grid_for(comps, 256), 256, 0, c->best.p, (const unsigned long long*)c->xw.p,
-           (const unsigned long long*)c->xuv.p, comps);
+  EdgeKey* keys = c->best.p;
+  if (V > 1) {
+    c->shard_keys.ensure((size_t)V * comps);
+    CK(cudaMemsetAsync(c->shard_keys.p, 0xff, (size_t)V * comps * sizeof(EdgeKey), c->stream));
+    keys = c->shard_keys.p;
   }
+  for (int g = 0; g < V; ++g) {
+    const long long s = (long long)c->rank * V + g;
+    traverse_dispatch(c, flags, keys + (size_t)g * comps, s * n / S, (s + 1) * n / S);
+  }
+  c->xw.ensure((size_t)V * comps);
+  c->xuv.ensure((size_t)V * comps);
+  for (int g = 0; g < V; ++g)
+    launch(c, k_split_keys, grid_for(comps, 256), 256, 0, (const EdgeKey*)(keys + (size_t)g * comps), comps,
+           c->xw.p + (size_t)g * comps);
+  allreduce_u64(c, c->xw.p, comps, V, comps, false);
+  for (int g = 0; g < V; ++g)
+    launch(c, k_mask_uv, grid_for(comps, 256), 256, 0, (const EdgeKey*)(keys + (size_t)g * comps),
+           (const unsigned long long*)c->xw.p, comps, c->xuv.p + (size_t)g * comps);
+  allreduce_u64(c, c->xuv.p, comps, V, comps, false);
+  launch(c, k_join_keys, grid_for(comps, 256), 256, 0, c->best.p, (const unsigned long long*)c->xw.p,
+         (const unsigned long long*)c->xuv.p, comps);
 }
 
 // Phase 4: collapse the successor graph; appends edges at `edge_base`, relabels.
@@ -838,7 +894,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   long long evals = c->host_counters[0];
   if (c->world > 1) {
     // total work counter over ranks (instrumentation only)
-    NK(ncclAllReduce(dev_counter(c, 0), dev_counter(c, 0), 1, ncclInt64, ncclSum, c->comm, c->stream));
+    allreduce_u64(c, reinterpret_cast<unsigned long long*>(dev_counter(c, 0)), 1, 1, 0, true);
     read_counters(c);
     evals = c->host_counters[0];
   }
@@ -933,8 +989,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     CK(cudaEventCreate(&c->ev_a));
     CK(cudaEventCreate(&c->ev_b));
     c->counters.ensure(kCounters);
-    if (world > 1) {
-      if (!nccl_id) fail(EMST_ERR_PARAM, "world > 1 needs an NCCL unique id");
+    if (world > 1 && nccl_id) {   // (without an id: a host exchange must be set, emst_context_set_exchange)
       ncclUniqueId id;
       memcpy(&id, nccl_id, sizeof(id));
       NK(ncclCommInitRank(&c->comm, world, id, rank));
@@ -960,7 +1015,7 @@ int emst_context_destroy(emst_context* c) {
   c->label.release(); c->bprefix.release(); c->big_tops.release(); c->top.release();
   c->front[0].release(); c->front[1].release(); c->core_slot.release(); c->core_tmp.release(); c->nfn_lb.release(); c->qlist.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
-  c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release();
+  c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release(); c->exch_host.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release(); c->tie_mid.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
@@ -979,7 +1034,34 @@ int emst_context_set_stream(emst_context* c, void* stream) {
 
 int emst_context_set_virtual_shards(emst_context* c, int shards) {
   if (!c || shards < 1 || shards > 64) return EMST_ERR_PARAM;
+  try {
+    set_device(c);
+    if (shards > 1 && c->world == 1 && !c->comm) {
+      // a 1-rank communicator: the virtual-shard runs take the same NCCL call path as N ranks
+      int dev = c->device;
+      NK(ncclCommInitAll(&c->comm, 1, &dev));
+    }
+  } catch (const Failure&) {
+    return EMST_ERR_NCCL;
+  }
   c->vshards = shards;
+  return EMST_OK;
+}
+
+int emst_context_set_exchange(emst_context* c, emst_exchange_fn fn, void* user) {
+  if (!c) return EMST_ERR_PARAM;
+  c->exch_fn = fn;
+  c->exch_user = user;
+  return EMST_OK;
+}
+
+int emst_context_wait_stream(emst_context* c, void* stream) {
+  if (!c) return EMST_ERR_PARAM;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (s == c->stream) return EMST_OK;
+  if (cudaSetDevice(c->device) != cudaSuccess) return EMST_ERR_CUDA;
+  if (cudaEventRecord(c->ev_a, s) != cudaSuccess) return EMST_ERR_CUDA;
+  if (cudaStreamWaitEvent(c->stream, c->ev_a, 0) != cudaSuccess) return EMST_ERR_CUDA;
   return EMST_OK;
 }
 
@@ -1120,22 +1202,48 @@ int emst_core_distances(emst_context* c, const float* pts, int64_t n, int32_t d,
 }
 
 
-int emst_morton_codes(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, uint64_t* codes_out,
-                      char* err, size_t errlen) {
+}  // extern "C"
+
+namespace {
+// Morton codes of the points into c->k0: against the tight scene box (k_scene,
+// which also checks finiteness), or against caller bounds (geometry.py:209-227:
+// lo and 1/extent in f64, 0 on a zero-extent axis; points outside are clamped).
+void codes_into_k0(emst_context* c, const float* dp, long long n, int d, const double* blo, const double* bhi) {
+  ensure_build(c, n, d);
+  CK(cudaMemsetAsync(c->scene.p, 0, sizeof(Scene), c->stream));
+  unsigned sg = (unsigned)std::min<long long>(grid_for(n, kSceneThreads), (long long)c->num_sms * 8);
+  if (d == 3) launch(c, k_scene<3>, sg, kSceneThreads, 0, dp, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
+  else launch(c, k_scene<2>, sg, kSceneThreads, 0, dp, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
+  Scene sc;
+  CK(cudaMemcpyAsync(&sc, c->scene.p, sizeof(Scene), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (sc.bad_row != 0x7fffffffffffffffll) fail(EMST_ERR_NONFINITE, "point %lld has a non-finite coordinate", sc.bad_row);
+  if (blo) {
+    for (int k = 0; k < 3; ++k) {
+      const double lo = k < d ? blo[k] : 0.0, hi = k < d ? bhi[k] : 0.0;
+      if (!(lo <= hi)) fail(EMST_ERR_PARAM, "bounds have lo > hi on axis %d", k);
+      const double ext = hi - lo;
+      sc.lo[k] = lo;
+      sc.inv[k] = ext > 0.0 ? 1.0 / ext : 0.0;
+    }
+    CK(cudaMemcpyAsync(c->scene.p, &sc, sizeof(Scene), cudaMemcpyHostToDevice, c->stream));
+  }
+  if (d == 3) launch(c, k_morton<3>, grid_for(n, 256), 256, 0, dp, n, (const Scene*)c->scene.p, c->k0.p);
+  else launch(c, k_morton<2>, grid_for(n, 256), 256, 0, dp, n, (const Scene*)c->scene.p, c->k0.p);
+}
+}  // namespace
+
+extern "C" {
+
+int emst_morton_codes(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, const double* bounds_lo,
+                      const double* bounds_hi, uint64_t* codes_out, char* err, size_t errlen) {
   try {
+    if (!c) fail(EMST_ERR_PARAM, "null context");
     set_device(c);
     check_shape(n, d);
+    if (!bounds_lo != !bounds_hi) fail(EMST_ERR_PARAM, "give both bound corners or neither");
     const float* dp = stage_points(c, pts, n, d, flags, nullptr);
-    ensure_build(c, n, d);
-    CK(cudaMemsetAsync(c->scene.p, 0, sizeof(Scene), c->stream));
-    unsigned sg = (unsigned)std::min<long long>(grid_for(n, kSceneThreads), (long long)c->num_sms * 8);
-    if (d == 3) {
-      launch(c, k_scene<3>, sg, kSceneThreads, 0, dp, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
-      launch(c, k_morton<3>, grid_for(n, 256), 256, 0, dp, n, (const Scene*)c->scene.p, c->k0.p);
-    } else {
-      launch(c, k_scene<2>, sg, kSceneThreads, 0, dp, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
-      launch(c, k_morton<2>, grid_for(n, 256), 256, 0, dp, n, (const Scene*)c->scene.p, c->k0.p);
-    }
+    codes_into_k0(c, dp, n, d, bounds_lo, bounds_hi);
     CK(cudaMemcpyAsync(codes_out, c->k0.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return EMST_OK;
@@ -1145,10 +1253,36 @@ int emst_morton_codes(emst_context* c, const float* pts, int64_t n, int32_t d, i
   }
 }
 
-int emst_build(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t* perm, int64_t* left,
-               int64_t* right, int64_t* parent, int64_t* leaf_parent, float* box_lo, float* box_hi, char* err,
-               size_t errlen) {
+int emst_sort_by_morton(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, const double* bounds_lo,
+                        const double* bounds_hi, int64_t* perm_out, char* err, size_t errlen) {
   try {
+    if (!c) fail(EMST_ERR_PARAM, "null context");
+    set_device(c);
+    check_shape(n, d);
+    if (!bounds_lo != !bounds_hi) fail(EMST_ERR_PARAM, "give both bound corners or neither");
+    const float* dp = stage_points(c, pts, n, d, flags, nullptr);
+    codes_into_k0(c, dp, n, d, bounds_lo, bounds_hi);
+    unsigned long long* keys;
+    unsigned* order;
+    radix_sort(c, n, d == 3 ? 63 : 62, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
+    DevBuf<long long> wide;
+    wide.ensure(n);
+    launch(c, k_u32_to_i64, grid_for(n, 256), 256, 0, (const unsigned*)order, (long long)n, wide.p);
+    CK(cudaMemcpyAsync(perm_out, wide.p, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    wide.release();
+    return EMST_OK;
+  } catch (const Failure& f) {
+    if (c) cudaStreamSynchronize(c->stream);
+    return finish(f, err, errlen);
+  }
+}
+
+int emst_build(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t* perm, int64_t* left,
+               int64_t* right, int64_t* parent, int64_t* leaf_parent, float* box_lo, float* box_hi,
+               int64_t* sweep_order, int64_t* sweep_starts, int64_t* n_starts, char* err, size_t errlen) {
+  try {
+    if (!c) fail(EMST_ERR_PARAM, "null context");
     set_device(c);
     check_shape(n, d);
     const float* dp = stage_points(c, pts, n, d, flags, nullptr);
@@ -1183,6 +1317,37 @@ int emst_build(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t 
     CK(cudaStreamSynchronize(c->stream));
     for (long long i = 0; i < n; ++i) perm[i] = hperm[i];
     if (n == 1) leaf_parent[0] = -1;
+    if (sweep_order && sweep_starts && n_starts) {
+      // the level schedule: heights by arrival climb, stable sort of the heights (bvh.py:204-238, 293-302)
+      *n_starts = 1;
+      sweep_starts[0] = 0;
+      if (m > 0) {
+        DevBuf<unsigned> height;
+        height.ensure(m);
+        CK(cudaMemsetAsync(height.p, 0, m * sizeof(unsigned), c->stream));
+        CK(cudaMemsetAsync(c->arrivals.p, 0, m * sizeof(unsigned), c->stream));
+        launch(c, k_node_heights, grid_for(n, 256), 256, 0, (const int*)c->leaf_parent.p, (const int*)c->node_parent.p,
+               (long long)n, c->arrivals.p, height.p);
+        launch(c, k_u32_to_u64, grid_for(m, 256), 256, 0, (const unsigned*)height.p, m, c->k0.p);
+        unsigned long long* hs;
+        unsigned* order;
+        radix_sort(c, m, 32, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &hs, &order);
+        DevBuf<long long> out;
+        out.ensure(2 * m + 1);
+        launch(c, k_level_starts, grid_for(m, 256), 256, 0, (const unsigned long long*)hs, (const unsigned*)order, m,
+               out.p + m, out.p);
+        unsigned long long hmax = 0;
+        CK(cudaMemcpyAsync(&hmax, hs + (m - 1), sizeof(hmax), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(sweep_order, out.p, m * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        if (hmax < 1 || hmax > (unsigned long long)m) fail(EMST_ERR_COUNT, "node height %llu out of range", hmax);
+        CK(cudaMemcpyAsync(sweep_starts, out.p + m, (hmax + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        *n_starts = (int64_t)hmax + 1;
+        height.release();
+        out.release();
+      }
+    }
     tmp.release();
     boxes.release();
     return EMST_OK;
@@ -1366,13 +1531,27 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
     ensure_rounds(c, n);
     c->iperm.ensure(n);
     c->counters.ensure(kCounters);
+    if (s > n) fail(EMST_ERR_PARAM, "%lld representatives for %lld points", (long long)s, (long long)n);
     std::vector<int> dense(n, -1), lab(n);
-    for (long long k = 0; k < s; ++k) dense[reps[k]] = (int)k;
-    for (long long i = 0; i < n; ++i) lab[i] = dense[labels[i]];
+    for (long long k = 0; k < s; ++k) {
+      const long long r = reps[k];
+      if (r < 0 || r >= n) fail(EMST_ERR_PARAM, "representative %lld out of range [0, %lld)", r, (long long)n);
+      if (dense[r] >= 0) fail(EMST_ERR_PARAM, "representative %lld listed twice", r);
+      dense[r] = (int)k;
+    }
+    for (long long i = 0; i < n; ++i) {
+      const long long l = labels[i];
+      if (l < 0 || l >= n || dense[l] < 0)
+        fail(EMST_ERR_PARAM, "label %lld of point %lld is not a listed representative", l, i);
+      lab[i] = dense[l];
+    }
     std::vector<EdgeKey> keys(s);
     for (long long k = 0; k < s; ++k) {
       long long r = reps[k];
       if (best_v[r] < 0) { keys[k].uv = ~0ull; keys[k].w = ~0ull; continue; }
+      if (best_u[r] < 0 || best_u[r] >= n || best_v[r] >= n)
+        fail(EMST_ERR_PARAM, "edge (%lld, %lld) of component %lld out of range", (long long)best_u[r],
+             (long long)best_v[r], r);
       keys[k].uv = ((unsigned long long)best_u[r] << 32) | (unsigned long long)best_v[r];
       memcpy(&keys[k].w, &best_w[r], 8);
     }

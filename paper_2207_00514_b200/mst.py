@@ -21,7 +21,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .bvh import Bvh, _device_points
+from .bvh import Bvh, _device_points, context_for
 from .errors import (
     DimensionMismatchError,
     InternalInvariantViolation,
@@ -160,6 +160,15 @@ def _resolve_metric(metric) -> tuple[str, CoreDistances | None]:
     raise InvalidParameterError(f"unknown metric {metric!r}")
 
 
+def _raise_call(rc: int, e, ctx: _lib.Context) -> None:
+    """raise_for, re-raising a host-exchange callback's own exception first."""
+    err = getattr(ctx, "exchange_error", None)
+    if rc and err is not None:
+        ctx.exchange_error = None
+        raise err
+    _lib.raise_for(rc, e)
+
+
 def _host_outputs(m: int):
     """(m, 2) int64 and (m,) float64 host arrays for the results.
 
@@ -212,7 +221,7 @@ def boruvka_emst(points, metric="euclidean", k_pts: int = 1, *, threads: int = 0
     ne = n - 1
     edges, weights = _host_outputs(max(ne, 1))
     st = _lib.Stats()
-    ctx = context if context is not None else _lib.default_context()
+    ctx = context_for(keep, context)
     e = _lib.err_buf()
     with ctx.lock:
         if kind == "mrd":
@@ -221,7 +230,7 @@ def boruvka_emst(points, metric="euclidean", k_pts: int = 1, *, threads: int = 0
         else:
             rc = _lib.load().emst_boruvka(ctx.handle, p, n, d, flags, edges.ctypes.data, weights.ctypes.data,
                                           ctypes.byref(st), e, len(e))
-    _lib.raise_for(rc, e)
+    _raise_call(rc, e, ctx)
     edges = edges[:ne]
     weights = weights[:ne]
     total = time.perf_counter() - t_start
@@ -367,16 +376,27 @@ def boruvka_emst_device(points, edges_out, weights_out, *, subtree_skip: bool = 
     if not (isinstance(points, torch.Tensor) and points.is_cuda and points.dtype == torch.float32):
         raise InvalidParameterError("points must be a CUDA float32 tensor")
     pts = points.contiguous()
+    if pts.ndim != 2:
+        raise DimensionMismatchError(f"points must be (n, d), got shape {tuple(pts.shape)}")
     n, d = int(pts.shape[0]), int(pts.shape[1])
-    if edges_out.shape != (max(n - 1, 0), 2) or weights_out.shape != (max(n - 1, 0),):
-        raise DimensionMismatchError("output tensors must be (n-1, 2) int64 and (n-1,) float64")
+    for name, t, dtype, shape in (("edges_out", edges_out, torch.int64, (max(n - 1, 0), 2)),
+                                  ("weights_out", weights_out, torch.float64, (max(n - 1, 0),))):
+        if not isinstance(t, torch.Tensor) or t.dtype != dtype or not t.is_cuda:
+            raise InvalidParameterError(f"{name} must be a CUDA {dtype} tensor")
+        if t.device != pts.device:
+            raise InvalidParameterError(f"{name} is on {t.device}, the points on {pts.device}")
+        if tuple(t.shape) != shape:
+            raise DimensionMismatchError(f"{name} must have shape {shape}, got {tuple(t.shape)}")
+        if not t.is_contiguous():
+            raise InvalidParameterError(f"{name} must be contiguous")
     flags = _lib.POINTS_ON_DEVICE | _lib.OUTPUT_ON_DEVICE
     flags |= (_lib.SUBTREE_SKIP if subtree_skip else 0) | (_lib.UPPER_BOUNDS if upper_bound_seeding else 0)
     st = _lib.Stats()
-    ctx = context if context is not None else _lib.default_context()
+    ctx = context_for(pts, context)
+    # the outputs may have been allocated (or still be read) on torch's stream: covered by the same wait
     e = _lib.err_buf()
     with ctx.lock:
         rc = _lib.load().emst_boruvka(ctx.handle, pts.data_ptr(), n, d, flags, edges_out.data_ptr(),
                                       weights_out.data_ptr(), ctypes.byref(st), e, len(e))
-    _lib.raise_for(rc, e)
+    _raise_call(rc, e, ctx)
     return st

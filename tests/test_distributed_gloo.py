@@ -1,9 +1,11 @@
-"""World-size-2 CPU tests (gloo) of the multi-GPU host logic.
+"""World-size-2/3 CPU tests (gloo) of the multi-GPU host logic.
 
 Covers what the N>1 path adds on top of the single-GPU kernels: the Morton
 shard plan, the NCCL-id rendezvous over torch.distributed, and the exactness
-of the two-phase min exchange (checked on oracle shards, since there is no GPU
-here).  The native NCCL path itself runs in bench.py under torchrun.
+of the two-phase min exchange through the host all-reduce the library calls
+back into (distributed.host_allreduce, checked on oracle shards since there is
+no GPU here).  tests/test_gpu_multirank.py runs the native path itself: N
+processes, each with its own context, sharding the traversal on one GPU.
 """
 
 import os
@@ -15,6 +17,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import paper_2207_00514_b200 as E
 from paper_2207_00514_b200 import distributed as D
 
 
@@ -36,12 +39,17 @@ def test_shard_ranges_partition_slots():
 
 
 def _keys(bu, bv, bw):
-    w = torch.from_numpy(bw.copy()).view(torch.int64)
-    uv = torch.from_numpy(np.where(bv >= 0, (bu << 32) | np.maximum(bv, 0), np.iinfo(np.int64).max))
-    return w, uv
+    """The device's EdgeKey halves: f64 weight bits, u << 32 | v; all-ones where none (k_split_keys' input)."""
+    w = np.where(bv >= 0, bw.view(np.uint64), np.uint64(~np.uint64(0)))
+    uv = np.where(bv >= 0, (bu.astype(np.uint64) << np.uint64(32)) | np.maximum(bv, 0).astype(np.uint64),
+                  np.uint64(~np.uint64(0)))
+    return w.astype(np.uint64), uv.astype(np.uint64)
 
 
 def _worker(rank, world, port, case, out):
+    """One rank: oracle keys of its Morton shard, then the two-phase exchange through the host all-reduce
+    the native library calls back into (distributed.host_allreduce), with the split / mask / join steps of
+    csrc/boruvka.cuh restated in numpy."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -52,17 +60,23 @@ def _worker(rank, world, port, case, out):
         b, e = D.shard_range(n, rank, world)
         bu, bv, bw, _ = orc.find_edges(pts, labels, il, ub, q_begin=b, q_end=e)
         w, uv = _keys(bu, bv, bw)
-        w_min, uv_min = D.exchange_component_minima(w, uv)
+        allreduce = D.host_allreduce()
+        xw = w.copy()                                        # k_split_keys
+        allreduce(xw, E._lib.EXCHANGE_MIN)                   # phase A
+        xuv = np.where(w == xw, uv, np.uint64(~np.uint64(0)))  # k_mask_uv
+        allreduce(xuv, E._lib.EXCHANGE_MIN)                  # phase B
+        total = np.array([np.uint64(rank + 1)], np.uint64)
+        allreduce(total, E._lib.EXCHANGE_SUM)
         nid = D.broadcast_nccl_id()
         if rank == 0:
-            np.savez(out, w=w_min.numpy(), uv=uv_min.numpy(), nid=np.frombuffer(nid, np.uint8))
+            np.savez(out, w=xw, uv=xuv, total=total, nid=np.frombuffer(nid, np.uint8))
         else:
             np.savez(out + f".{rank}", nid=np.frombuffer(nid, np.uint8))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
+@pytest.mark.parametrize("world", [2, 3])
 def test_two_phase_exchange_is_exact_over_gloo(small_golden, tmp_path, world):
     arrays, _ = small_golden
     name = "blobs2d_tie_20000"   # 2D lattice-like data: many exact weight ties
@@ -76,6 +90,7 @@ def test_two_phase_exchange_is_exact_over_gloo(small_golden, tmp_path, world):
         got = np.load(out)
         reps = arrays[p + "reps"]
         w = got["w"].view(np.float64)
+        assert int(got["total"][0]) == world * (world + 1) // 2
         assert np.array_equal(w[reps], arrays[p + "best_w"])
         assert np.array_equal(got["uv"][reps] >> 32, arrays[p + "best_u"])
         assert np.array_equal(got["uv"][reps] & 0xFFFFFFFF, arrays[p + "best_v"])
