@@ -81,6 +81,8 @@ typedef struct emst_stats {
   int64_t round_found[64];      /* per round: queries that found a candidate edge */
   int64_t round_skipped[64];    /* per round: queries settled before any node visit */
   double total_weight;          /* float(np.sum(weights)): numpy's pairwise order, on the device */
+  double host_in_ms;            /* host wall time handing the points over (host-pointer entry) */
+  double host_out_ms;           /* host wall time bringing the edges / weights back */
 } emst_stats;
 
 typedef struct emst_context emst_context;

@@ -77,6 +77,8 @@ class Stats(ctypes.Structure):
         ("round_found", ctypes.c_int64 * 64),
         ("round_skipped", ctypes.c_int64 * 64),
         ("total_weight", ctypes.c_double),
+        ("host_in_ms", ctypes.c_double),
+        ("host_out_ms", ctypes.c_double),
     ]
 
 
@@ -92,6 +94,7 @@ EXPORTS = (
     "emst_boruvka_mrd",
     "emst_core_distances",
     "emst_morton_codes",
+    "emst_sort_by_morton",
     "emst_build",
     "emst_reduce_labels",
     "emst_compute_upper_bounds",
@@ -144,8 +147,9 @@ def load():
         L.emst_boruvka.argtypes = [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(Stats), cp, sz]
         L.emst_boruvka_mrd.argtypes = [vp, vp, i64, i32, i32, i64, vp, vp, vp, ctypes.POINTER(Stats), cp, sz]
         L.emst_core_distances.argtypes = [vp, vp, i64, i32, i32, i64, vp, cp, sz]
-        L.emst_morton_codes.argtypes = [vp, vp, i64, i32, i32, vp, cp, sz]
-        L.emst_build.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, cp, sz]
+        L.emst_morton_codes.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, cp, sz]
+        L.emst_sort_by_morton.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, cp, sz]
+        L.emst_build.argtypes = [vp, vp, i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, cp, sz]
         L.emst_reduce_labels.argtypes = [vp, vp, i64, i32, vp, vp, cp, sz]
         L.emst_compute_upper_bounds.argtypes = [vp, vp, i64, i32, vp, vp, vp, cp, sz]
         L.emst_find_component_outgoing_edges.argtypes = [vp, vp, i64, i32, vp, vp, vp, i32, vp, vp, vp, vp, cp, sz]

@@ -8,12 +8,21 @@ same boxes -- tests/test_gpu_parity.py compares them array for array.
 
 from __future__ import annotations
 
+import ctypes
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _lib
-from .errors import InvalidIndexError
+from .errors import (
+    DimensionMismatchError,
+    InvalidCoordinateError,
+    InvalidIndexError,
+    InvalidParameterError,
+    TraversalStackOverflowError,
+    UnsupportedDimensionError,
+)
 from .geometry import Aabb, as_point_array, check_shape
 
 STACK_CAPACITY = 64   # bvh.py:36
@@ -36,6 +45,10 @@ class Bvh:
     leaf_parent: np.ndarray
     box_lo: np.ndarray
     box_hi: np.ndarray
+    # bottom-up level schedule (bvh.py:60-63): nodes sweep_order[sweep_starts[k]:sweep_starts[k + 1]]
+    # have height k + 1
+    sweep_order: np.ndarray | None = None
+    sweep_starts: np.ndarray | None = None
     # the points the GPU built this tree from (the building blocks rebuild from them)
     points: np.ndarray | None = field(default=None, repr=False, compare=False)
 
@@ -117,14 +130,55 @@ def context_for(keep, context=None) -> _lib.Context:
     return context if context is not None else _lib.default_context()
 
 
-def morton_codes(points) -> np.ndarray:
-    """Morton codes with the tight scene bounds, computed on the GPU (geometry.py:209-227)."""
+def _bounds_arrays(bounds: Aabb | None, d: int):
+    """(keep-alive, lo pointer, hi pointer) of an Aabb for the C ABI; NULLs for the tight scene box."""
+    if bounds is None:
+        return None, None, None
+    if not isinstance(bounds, Aabb):
+        raise InvalidParameterError(f"bounds must be an Aabb, got {type(bounds).__name__}")
+    if bounds.dim != d:
+        raise DimensionMismatchError("bounds dimension differs from point dimension")
+    lo = np.ascontiguousarray(bounds.lo, np.float64)
+    hi = np.ascontiguousarray(bounds.hi, np.float64)
+    return (lo, hi), lo.ctypes.data, hi.ctypes.data
+
+
+def morton_codes(points, bounds: Aabb | None = None) -> np.ndarray:
+    """Morton codes quantised against `bounds` (the tight scene box by default), on the GPU
+    (geometry.py:209-227): 63 bits in 3D, 62 in 2D; points outside `bounds` are clamped into it."""
     p, n, d, flags, keep = _device_points(points)
+    bkeep, blo, bhi = _bounds_arrays(bounds, d)
     out = np.empty(n, np.uint64)
     ctx = context_for(keep)
     e = _lib.err_buf()
     with ctx.lock:
-        rc = _lib.load().emst_morton_codes(ctx.handle, p, n, d, flags, out.ctypes.data, e, len(e))
+        rc = _lib.load().emst_morton_codes(ctx.handle, p, n, d, flags, blo, bhi, out.ctypes.data, e, len(e))
+    _lib.raise_for(rc, e)
+    return out
+
+
+def morton_encode(point, bounds: Aabb) -> int:
+    """Morton code of one point within `bounds`, clamped into it (geometry.py:230-244)."""
+    p = np.asarray(point, dtype=np.float64)
+    if p.ndim != 1:
+        raise UnsupportedDimensionError("morton_encode takes a single point")
+    if p.shape[0] != bounds.dim:
+        raise DimensionMismatchError("point dimension differs from bounds dimension")
+    if not np.isfinite(p).all():
+        raise InvalidCoordinateError("point has a non-finite coordinate")
+    return int(morton_codes(p.astype(np.float32)[None, :], bounds)[0])
+
+
+def sort_by_morton(points, bounds: Aabb | None = None) -> np.ndarray:
+    """Permutation ordering the points by (Morton code, original index) (geometry.py:247-254): the
+    solve's stable onesweep radix sort on the GPU."""
+    p, n, d, flags, keep = _device_points(points)
+    bkeep, blo, bhi = _bounds_arrays(bounds, d)
+    out = np.empty(n, np.int64)
+    ctx = context_for(keep)
+    e = _lib.err_buf()
+    with ctx.lock:
+        rc = _lib.load().emst_sort_by_morton(ctx.handle, p, n, d, flags, blo, bhi, out.ctypes.data, e, len(e))
     _lib.raise_for(rc, e)
     return out
 
@@ -140,17 +194,91 @@ def build(points) -> Bvh:
     leaf_parent = np.empty(n, np.int64)
     box_lo = np.empty((max(m, 1), d), np.float32)
     box_hi = np.empty((max(m, 1), d), np.float32)
+    order = np.empty(max(m, 1), np.int64)
+    starts = np.empty(n, np.int64)
+    n_starts = ctypes.c_int64(0)
     ctx = context_for(keep)
     e = _lib.err_buf()
     with ctx.lock:
         rc = _lib.load().emst_build(ctx.handle, p, n, d, flags, perm.ctypes.data, left.ctypes.data, right.ctypes.data,
                                     parent.ctypes.data, leaf_parent.ctypes.data, box_lo.ctypes.data,
-                                    box_hi.ctypes.data, e, len(e))
+                                    box_hi.ctypes.data, order.ctypes.data, starts.ctypes.data,
+                                    ctypes.byref(n_starts), e, len(e))
     _lib.raise_for(rc, e)
     host = keep if isinstance(keep, np.ndarray) else keep.detach().cpu().numpy()
-    return Bvh(n, d, perm, left[:m], right[:m], parent[:m], leaf_parent, box_lo[:m], box_hi[:m], host)
+    return Bvh(n, d, perm, left[:m], right[:m], parent[:m], leaf_parent, box_lo[:m], box_hi[:m], order[:m],
+               starts[:n_starts.value].copy(), host)
 
 
-def sort_by_morton(points) -> np.ndarray:
-    """Z-order permutation with index tie-break (geometry.py:247-254), from the GPU sort."""
-    return build(points).leaf_perm
+def _ref_bound(bvh: Bvh, coords: np.ndarray, q: np.ndarray, ref: int) -> float:
+    """f64 distance from q to a leaf point (ref >= n - 1) or to an internal node's box, axes summed in
+    order without fused operations (bvh.py:267-290)."""
+    m = bvh.num_internal
+    acc = 0.0
+    if ref >= m:
+        p = coords[int(bvh.leaf_perm[ref - m])]
+        for k in range(bvh.dim):
+            g = float(q[k]) - float(p[k])
+            acc += g * g
+    else:
+        lo, hi = bvh.box_lo[ref], bvh.box_hi[ref]
+        for k in range(bvh.dim):
+            x = float(q[k])
+            g = float(lo[k]) - x if x < float(lo[k]) else (x - float(hi[k]) if x > float(hi[k]) else 0.0)
+            acc += g * g
+    return math.sqrt(acc)
+
+
+def traverse_nearest(bvh: Bvh, points, query, *, on_leaf, prune=None, radius: float = math.inf) -> float:
+    """Constrained nearest-neighbour walk from the root with caller callbacks (bvh.py:343-418).
+
+    Host-side: the callbacks are arbitrary Python, so this walk runs on the CPU over the
+    GPU-built arrays (the solve's own traversal never comes here).  Same contract as the
+    reference: depth first, nearer child first (the left one on a tie), ``on_leaf(point, dist)``
+    may return a smaller radius, ``prune(ref, lower_bound, radius)`` may veto an entry (default:
+    drop it when lower_bound > radius), at most STACK_CAPACITY entries stacked.
+    """
+    coords = as_point_array(points)
+    if coords.shape != (bvh.num_points, bvh.dim):
+        raise DimensionMismatchError("points array does not match the hierarchy")
+    q = np.asarray(query, dtype=np.float64)
+    if q.shape != (bvh.dim,):
+        raise DimensionMismatchError("query dimension differs from hierarchy dimension")
+    m = bvh.num_internal
+    start = 0 if m > 0 else m   # one point: the root is the leaf itself
+    pending = [(start, _ref_bound(bvh, coords, q, start))]
+    while pending:
+        ref, lb = pending.pop()
+        veto = prune(ref, lb, radius) if prune is not None else lb > radius
+        if veto:
+            continue
+        if ref >= m:
+            got = on_leaf(int(bvh.leaf_perm[ref - m]), lb)
+            if got is not None:
+                radius = float(got)
+            continue
+        kids = [(int(bvh.left[ref]), 0), (int(bvh.right[ref]), 1)]
+        bounds = [(_ref_bound(bvh, coords, q, c), side, c) for c, side in kids]
+        bounds.sort()   # nearer first; equal bounds keep the left child nearer
+        if len(pending) + 2 > STACK_CAPACITY:
+            raise TraversalStackOverflowError(f"traversal exceeded {STACK_CAPACITY} stacked nodes")
+        for b, _, c in reversed(bounds):   # the nearer one ends on top
+            pending.append((c, b))
+    return radius
+
+
+def for_each_leaf_to_root(bvh: Bvh, visit) -> None:
+    """Bottom-up rendezvous over the internal nodes (bvh.py:421-440): every leaf climbs; the first
+    arrival at a node stops, the second calls ``visit(node)`` (so a node is visited once, after both
+    subtrees) and climbs on unless ``visit`` returned False.  Host-side, for caller callbacks; the
+    GPU's refit and height kernels run the same protocol with atomics."""
+    seen = np.zeros(bvh.num_internal, dtype=bool)
+    for slot in range(bvh.num_points):
+        node = int(bvh.leaf_parent[slot])
+        while node >= 0:
+            if not seen[node]:
+                seen[node] = True
+                break
+            if visit(node) is False:
+                break
+            node = int(bvh.parent[node])

@@ -753,6 +753,16 @@ __global__ void k_edge_emit(const unsigned long long* __restrict__ w, const unsi
   weights[i] = __longlong_as_double((long long)w[i]);
 }
 
+// the host-pointer entry's variant: packed (u << 32 | v) rows, 8 bytes per edge over PCIe (hostio.h)
+__global__ void k_edge_emit_packed(const unsigned long long* __restrict__ w, const unsigned* __restrict__ order,
+                                   const unsigned long long* __restrict__ euv, long long ne,
+                                   unsigned long long* __restrict__ packed, double* __restrict__ weights) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= ne) return;
+  packed[i] = euv[order[i]];
+  weights[i] = __longlong_as_double((long long)w[i]);
+}
+
 // ----------------------------------------------------- total weight (numpy order)
 // float(np.sum(weights)) (mst.py:749) reproduced bit for bit: numpy adds a
 // float64 array by pairwise summation -- blocks of <= 128 with 8 interleaved

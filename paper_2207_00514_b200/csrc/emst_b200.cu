@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -19,6 +20,7 @@
 #include "core.cuh"
 #include "build.cuh"
 #include "radix_sort.cuh"
+#include "hostio.h"
 #include "textio.h"
 #include "scan.cuh"
 
@@ -122,8 +124,12 @@ struct emst_context {
   emst_exchange_fn exch_fn = nullptr;   // host exchange (world > 1 without NCCL)
   void* exch_user = nullptr;
   HostBuf<unsigned long long> exch_host;
+  emst_host::Stager stager;          // pageable host <-> HBM pipeline of the host-pointer entry
+  bool staging = true;               // EMST_STAGE=0: plain cudaMemcpyAsync of pageable memory (A/B)
+  bool packed_out = true;            // EMST_PACKED=0: int64 rows straight from the device (A/B)
   cudaStream_t stream = nullptr;
   cudaStream_t own_stream = nullptr;
+  cudaStream_t copy_stream = nullptr;   // second copy engine: the weights D2H beside the edge chunks
   long long launches = 0;
   double traverse_ms = 0.0;
   long long traverse_launches = 0, traverse_queries = 0;
@@ -414,7 +420,15 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
 const float* stage_points(emst_context* c, const float* pts, long long n, int d, int flags, emst_stats* st) {
   if (flags & EMST_POINTS_ON_DEVICE) return pts;
   c->pts.ensure((size_t)n * d);
-  CK(cudaMemcpyAsync(c->pts.p, pts, (size_t)n * d * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+  const size_t bytes = (size_t)n * d * sizeof(float);
+  const auto t0 = std::chrono::steady_clock::now();
+  if (c->staging && bytes >= (4u << 20) && !emst_host::is_pinned(pts)) {
+    CK(c->stager.init());
+    CK(c->stager.h2d(c->pts.p, pts, bytes, c->stream));
+  } else {
+    CK(cudaMemcpyAsync(c->pts.p, pts, bytes, cudaMemcpyHostToDevice, c->stream));
+  }
+  if (st) st->host_in_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   if (st) st->h2d_bytes += (long long)n * d * sizeof(float);
   return c->pts.p;
 }
@@ -684,7 +698,7 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
 // sort on the weight bits (passes whose digit is constant are skipped); equal
 // weights are then put in (u, v) order: runs of up to kShortTie edges by the
 // thread at the run start, anything longer by the exact two-key LSD sort.
-void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* w_dst) {
+void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* w_dst, bool packed = false) {
   if (ne <= 0) return;
   unsigned long long* keys;
   unsigned* order;
@@ -724,8 +738,12 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
     launch(c, k_edge_fix_long, long_runs, 1024, 0, (const int2*)c->tie_runs.p, (const unsigned long long*)c->euv.p,
            order);
   }
-  launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, (const unsigned*)order,
-         (const unsigned long long*)c->euv.p, ne, edges_dst, w_dst);
+  if (packed)
+    launch(c, k_edge_emit_packed, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, (const unsigned*)order,
+           (const unsigned long long*)c->euv.p, ne, reinterpret_cast<unsigned long long*>(edges_dst), w_dst);
+  else
+    launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, (const unsigned*)order,
+           (const unsigned long long*)c->euv.p, ne, edges_dst, w_dst);
 }
 
 // float(np.sum(weights)) on the device in numpy's summation order.
@@ -809,7 +827,7 @@ void prepare_cores(emst_context* c, long long n, long long k_pts, const double* 
 }
 
 void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags, long long* edges_dev,
-           double* w_dev, emst_stats* st, long long k_pts = 1, const double* core_host = nullptr) {
+           double* w_dev, emst_stats* st, long long k_pts = 1, const double* core_host = nullptr, bool packed = false) {
   cudaEvent_t t0, t1, t2, t3;
   CK(cudaEventCreate(&t0));
   CK(cudaEventCreate(&t1));
@@ -886,7 +904,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     if (st->num_counts < 64) st->component_counts[st->num_counts++] = comps;
   }
   if (edges != n - 1) fail(EMST_ERR_COUNT, "collected %lld edges for %lld points", edges, n);
-  sort_and_emit(c, edges, edges_dev, w_dev);
+  sort_and_emit(c, edges, edges_dev, w_dev, packed);
   total_weight(c, w_dev, edges, st);
   CK(cudaEventRecord(t2, c->stream));
   CK(cudaEventSynchronize(t2));
@@ -979,10 +997,13 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (const char* t = getenv("EMST_IPERM_PARTS")) c->iperm_parts = atoi(t);
     if (const char* t = getenv("EMST_LIST_SKIP")) c->list_skip = atof(t);
     if (const char* t = getenv("EMST_SINGLE_KERNEL")) c->single_kernel = atoi(t) != 0;
+    if (const char* t = getenv("EMST_STAGE")) c->staging = atoi(t) != 0;
+    if (const char* t = getenv("EMST_PACKED")) c->packed_out = atoi(t) != 0;
     c->rank = rank;
     c->world = world;
     set_device(c);
     CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     c->stream = c->own_stream;
     CK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     CK(cudaMallocHost(&c->host_counters, kCounters * sizeof(long long)));
@@ -1016,12 +1037,14 @@ int emst_context_destroy(emst_context* c) {
   c->front[0].release(); c->front[1].release(); c->core_slot.release(); c->core_tmp.release(); c->nfn_lb.release(); c->qlist.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release(); c->exch_host.release();
+  c->stager.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release(); c->tie_mid.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   delete c;
   return EMST_OK;
 }
@@ -1114,12 +1137,42 @@ int boruvka_impl(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
       st->component_counts[0] = 1;
       st->num_counts = 1;
     } else {
-      solve(c, dp, n, d, flags, edst, wdst, st, k_pts, core_host);
+      const bool host_out = !(flags & EMST_OUTPUT_ON_DEVICE);
+      const bool packed = host_out && c->staging && c->packed_out;
+      solve(c, dp, n, d, flags, edst, wdst, st, k_pts, core_host, packed);
       c->core = nullptr;
-      if (!(flags & EMST_OUTPUT_ON_DEVICE)) {
+      if (host_out) CK(cudaStreamSynchronize(c->stream));   // (host_out_ms: the transfers alone)
+      const auto t_out0 = std::chrono::steady_clock::now();
+      if (packed) {
+        // (u << 32 | v) rows widened on the host while the next chunk is in flight (hostio.h)
+        CK(c->stager.init());
+        const bool w_direct = emst_host::is_pinned(weights_out);
+        if (w_direct) {   // page-locked destination: straight DMA, concurrent with the edge chunks below
+          CK(cudaEventRecord(c->ev_b, c->stream));
+          CK(cudaStreamWaitEvent(c->copy_stream, c->ev_b, 0));
+          CK(cudaMemcpyAsync(weights_out, wdst, ne * sizeof(double), cudaMemcpyDeviceToHost, c->copy_stream));
+        }
+        int64_t* eo = edges_out;
+        CK(c->stager.d2h(edst, (size_t)ne, sizeof(unsigned long long), c->stream,
+                         [eo](size_t at, const unsigned char* src, size_t cnt) {
+                           emst_host::widen_pairs(reinterpret_cast<const unsigned long long*>(src), cnt, eo + 2 * at);
+                         }));
+        if (w_direct) {
+          CK(cudaStreamSynchronize(c->copy_stream));
+        } else {
+          double* wo = weights_out;
+          CK(c->stager.d2h(wdst, (size_t)ne, sizeof(double), c->stream,
+                           [wo](size_t at, const unsigned char* src, size_t cnt) { memcpy(wo + at, src, cnt * 8); }));
+        }
+        st->d2h_bytes += ne * (sizeof(unsigned long long) + sizeof(double));
+      } else if (host_out) {
         CK(cudaMemcpyAsync(edges_out, edst, 2 * ne * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(weights_out, wdst, ne * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         st->d2h_bytes += ne * (2 * sizeof(long long) + sizeof(double));
+      }
+      if (host_out) {
+        CK(cudaStreamSynchronize(c->stream));
+        st->host_out_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_out0).count();
       }
     }
     CK(cudaEventRecord(e1, c->stream));

@@ -230,6 +230,7 @@ def boruvka_emst(points, metric="euclidean", k_pts: int = 1, *, threads: int = 0
         else:
             rc = _lib.load().emst_boruvka(ctx.handle, p, n, d, flags, edges.ctypes.data, weights.ctypes.data,
                                           ctypes.byref(st), e, len(e))
+    ctx.last_stats = st
     _raise_call(rc, e, ctx)
     edges = edges[:ne]
     weights = weights[:ne]

@@ -14,6 +14,8 @@ Usage (needs a writable numba cache because the reference tree is read-only)::
 ``small`` writes ``tests/golden/small.npz`` + ``tests/golden/small.json`` (seconds);
 ``mrd`` writes ``tests/golden/mrd.npz`` + ``tests/golden/mrd.json``: the mutual-reachability
 metric (core distances for k_pts and the MSTs; reference metric.py / mst.py:638-644);
+``api`` writes ``tests/golden/api.npz`` + ``api.json``: the tree-level API (level schedule, Morton codes
+with caller bounds, traverse_nearest / for_each_leaf_to_root call sequences);
 ``large`` appends the full-size configurations of BASELINE.json to
 ``tests/golden/large.json`` (minutes: 10M-37M points on the host CPU).
 
@@ -309,10 +311,86 @@ def make_mrd():
         json.dump(meta, fh, indent=1, sort_keys=True)
 
 
+def _api_walks(emst, tree, pts, arrays, prefix):
+    """traverse_nearest / for_each_leaf_to_root call sequences for a few queries (bvh.py:343-440)."""
+    rng = np.random.default_rng(7)
+    qs = np.concatenate([pts[rng.integers(0, pts.shape[0], 4)].astype(np.float64),
+                         rng.random((2, pts.shape[1])) * 2 - 1])
+    arrays[prefix + "queries"] = qs
+    for j, q in enumerate(qs):
+        seen = []
+
+        def on_leaf(p, dist):
+            seen.append((p, dist))
+            return dist if dist > 0 else None   # nearest-neighbour shrink (ties stay visited)
+
+        r = emst.traverse_nearest(tree, pts, q, on_leaf=on_leaf)
+        arrays[prefix + f"walk{j}_pts"] = np.array([p for p, _ in seen], np.int64)
+        arrays[prefix + f"walk{j}_dist"] = np.array([d for _, d in seen], np.float64)
+        arrays[prefix + f"walk{j}_radius"] = np.array([r])
+        pruned = []
+
+        def prune(ref, lb, radius):
+            pruned.append((ref, lb))
+            return lb > 0.25 * (1 + (ref % 3))
+
+        got = []
+        r = emst.traverse_nearest(tree, pts, q, on_leaf=lambda p, d: got.append(p), prune=prune, radius=0.5)
+        arrays[prefix + f"prune{j}_refs"] = np.array([a for a, _ in pruned], np.int64)
+        arrays[prefix + f"prune{j}_lbs"] = np.array([b for _, b in pruned], np.float64)
+        arrays[prefix + f"prune{j}_pts"] = np.array(got, np.int64)
+    order = []
+    emst.for_each_leaf_to_root(tree, lambda v: order.append(v))
+    arrays[prefix + "sweep_visits"] = np.array(order, np.int64)
+    stop = []
+    emst.for_each_leaf_to_root(tree, lambda v: (stop.append(v), v % 5 != 0)[1])
+    arrays[prefix + "sweep_visits_stop"] = np.array(stop, np.int64)
+
+
+def make_api():
+    """Goldens of the tree-level public API around the hot path: the level schedule
+    (Bvh.sweep_order / sweep_starts), morton_codes / sort_by_morton with caller bounds, morton_encode,
+    traverse_nearest and for_each_leaf_to_root call sequences."""
+    emst = _import_reference()
+    arrays = {}
+    gen, _ = _generated_inputs(emst)
+    cases = dict(_tie_inputs())
+    cases.update({k: gen[k] for k in ("uniform2d_1000_s0", "normal3d_1000_s1", "blobs3d_3000_s2", "blobs2d_3000_s3")})
+    names = []
+    for name, pts in cases.items():
+        if pts.shape[0] < 2:
+            continue
+        names.append(name)
+        p = name + "/"
+        tree = emst.build(pts)
+        arrays[p + "points"] = pts
+        for f in ("leaf_perm", "left", "right", "parent", "leaf_parent", "box_lo", "box_hi"):
+            arrays[p + f] = getattr(tree, f)
+        arrays[p + "sweep_order"] = tree.sweep_order
+        arrays[p + "sweep_starts"] = tree.sweep_starts
+        d = pts.shape[1]
+        lo, hi = pts.min(0).astype(np.float64), pts.max(0).astype(np.float64)
+        ext = hi - lo
+        for tag, blo, bhi in (("inner", lo + 0.25 * ext, hi - 0.3 * ext), ("outer", lo - 1.5, hi + 0.75),
+                              ("flat", np.where(np.arange(d) == 0, lo, lo - 1), np.where(np.arange(d) == 0, lo, hi + 1))):
+            b = emst.Aabb(blo, bhi)
+            arrays[p + f"bounds_{tag}"] = np.stack([blo, bhi])
+            arrays[p + f"codes_{tag}"] = emst.morton_codes(pts, b)
+            arrays[p + f"perm_{tag}"] = emst.sort_by_morton(pts, b)
+            arrays[p + f"encode_{tag}"] = np.array([emst.morton_encode(x, b) for x in pts[:16]], np.uint64)
+        if name in ("uniform2d_1000_s0", "normal3d_1000_s1", "grid9", "lattice_dups_3d"):
+            _api_walks(emst, tree, pts, arrays, p)
+    np.savez_compressed(os.path.join(HERE, "api.npz"), **arrays)
+    with open(os.path.join(HERE, "api.json"), "w") as fh:
+        json.dump({"cases": names}, fh, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "small"
     if which == "small":
         make_small()
+    elif which == "api":
+        make_api()
     elif which == "mrd":
         make_mrd()
     else:

@@ -256,3 +256,109 @@ def test_search_switches_do_not_change_the_result(env, monkeypatch):
             assert got.iterations == ref.iterations and list(got.component_counts) == list(ref.component_counts)
     finally:
         ctx.close()
+
+
+def test_points_produced_on_another_stream_are_awaited():
+    """The library runs on its own stream; CUDA-tensor input produced by torch kernels still in flight
+    (queued behind a long matmul on torch's current stream) must be waited for, not read early."""
+    import torch
+    from oracle import oracle as orc
+    torch.manual_seed(0)
+    for _ in range(3):
+        a = torch.randn(8192, 8192, device="cuda")
+        for _ in range(6):
+            a = a @ a * 1e-2   # ~100 ms of queued work ahead of the points
+        pts = torch.rand(30000, 3, device="cuda") + a[:1, :1].nan_to_num(0.0, 0.0, 0.0) * 0   # after the chain
+        pts[17] = float("nan")   # an in-place edit right before the call must be seen
+        with pytest.raises(E.InvalidCoordinateError, match="point 17 "):
+            E.boruvka_emst(pts)
+        pts[17] = 0.5
+        got = E.boruvka_emst(pts)
+        ref = orc.boruvka_emst(pts.cpu().numpy())
+        assert np.array_equal(got.edges, ref.edges) and np.array_equal(got.weights, ref.weights)
+
+
+def test_device_entry_checks_its_outputs():
+    import torch
+    pts = torch.rand(1000, 3, device="cuda")
+    good_e = torch.empty((999, 2), dtype=torch.int64, device="cuda")
+    good_w = torch.empty((999,), dtype=torch.float64, device="cuda")
+    bad = [(torch.empty((999, 2), dtype=torch.int32, device="cuda"), good_w, E.InvalidParameterError),
+           (good_e, torch.empty((999,), dtype=torch.float32, device="cuda"), E.InvalidParameterError),
+           (torch.empty((999, 2), dtype=torch.int64), good_w, E.InvalidParameterError),
+           (torch.empty((2, 999), dtype=torch.int64, device="cuda").t(), good_w, E.InvalidParameterError),
+           (torch.empty((998, 2), dtype=torch.int64, device="cuda"), good_w, E.DimensionMismatchError)]
+    for e, w, exc in bad:
+        with pytest.raises(exc):
+            E.boruvka_emst_device(pts, e, w)
+    st = E.boruvka_emst_device(pts, good_e, good_w)
+    ref = E.boruvka_emst(pts.cpu().numpy())
+    assert np.array_equal(good_e.cpu().numpy(), ref.edges) and np.array_equal(good_w.cpu().numpy(), ref.weights)
+    assert st.iterations == ref.iterations
+
+
+@pytest.mark.parametrize("name", ["uniform3d_1m", "blobs3d_1m"])
+def test_device_resident_entry_matches_reference_digest(large_golden, name):
+    """The entry bench.py times (points and results in HBM) against the reference's digest."""
+    import torch
+    rec = large_golden[name]
+    s = rec["spec"]
+    pts = torch.from_numpy(E.generate(E.DatasetSpec(s["kind"], s["n"], s["d"], s["seed"]))).cuda()
+    n = pts.shape[0]
+    e = torch.empty((n - 1, 2), dtype=torch.int64, device="cuda")
+    w = torch.empty((n - 1,), dtype=torch.float64, device="cuda")
+    for _ in range(2):   # (the second call reuses the context's workspace)
+        st = E.boruvka_emst_device(pts, e, w)
+        assert digest(e.cpu().numpy(), w.cpu().numpy()) == rec["digest"]
+        assert st.iterations == rec["iterations"]
+        assert [st.component_counts[i] for i in range(st.num_counts)] == rec["component_counts"]
+
+
+def test_merge_components_rejects_bad_state():
+    pts = E.generate(E.DatasetSpec("uniform", 200, 2, seed=1))
+    tree = E.build(pts)
+    state = E.ComponentState.initial(tree)
+    E.compute_upper_bounds(state, tree.leaf_perm, pts)
+    E.reduce_labels(tree, state)
+    out = E.find_component_outgoing_edges(tree, pts, state)
+    bad = E.OutgoingEdges(out.reps[:-1], out.u, out.v, out.w, 0)   # a label with no representative
+    with pytest.raises(E.InvalidParameterError):
+        E.merge_components(E.ComponentState(state.labels.copy(), state.internal_labels, state.upper_bounds), bad)
+    oob = out.u.copy()
+    oob[out.reps[0]] = 10**6
+    with pytest.raises(E.InvalidParameterError):
+        E.merge_components(E.ComponentState(state.labels.copy(), state.internal_labels, state.upper_bounds),
+                           E.OutgoingEdges(out.reps, oob, out.v, out.w, 0))
+
+
+@pytest.mark.parametrize("env", [{}, {"EMST_STAGE": "0"}, {"EMST_PACKED": "0"}])
+def test_host_transfer_paths(large_golden, env, monkeypatch):
+    """The host-pointer entry's transfer variants (hostio.h): staged pageable input or plain cudaMemcpy,
+    packed (u << 32 | v) rows widened on the host or int64 rows from the device, weights straight into a
+    page-locked buffer or through the staging ring, 16-byte aligned or unaligned int64 rows."""
+    import ctypes
+    import torch
+    from paper_2207_00514_b200 import _lib
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rec = large_golden["uniform3d_1m"]
+    s = rec["spec"]
+    pts = E.generate(E.DatasetSpec(s["kind"], s["n"], s["d"], s["seed"]))
+    n = pts.shape[0]
+    ctx = E.Context(0)
+    try:
+        for pinned_in, offset, pinned_w in ((False, 0, True), (True, 1, False), (False, 1, False)):
+            src = torch.from_numpy(pts).pin_memory().numpy() if pinned_in else pts
+            ebuf = np.zeros(2 * (n - 1) + 2, np.int64)
+            edges = ebuf[offset:offset + 2 * (n - 1)]   # offset 1: 8-byte aligned only (scalar widening)
+            w = (torch.empty(n - 1, dtype=torch.float64, pin_memory=True).numpy() if pinned_w
+                 else np.empty(n - 1, np.float64))
+            st = _lib.Stats()
+            err = _lib.err_buf()
+            rc = _lib.load().emst_boruvka(ctx.handle, src.ctypes.data, n, 3, _lib.SUBTREE_SKIP | _lib.UPPER_BOUNDS,
+                                          edges.ctypes.data, w.ctypes.data, ctypes.byref(st), err, len(err))
+            _lib.raise_for(rc, err)
+            assert digest(edges.reshape(n - 1, 2), w) == rec["digest"], (env, pinned_in, offset, pinned_w)
+            assert ebuf[0] == 0 or offset == 0 and ebuf[-1] == 0   # nothing written outside the rows
+    finally:
+        ctx.close()

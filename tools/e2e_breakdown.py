@@ -1,26 +1,25 @@
-"""Where the end-to-end call spends its time (developer tool)."""
-import time, ctypes
-import numpy as np, torch
-import paper_2207_00514_b200 as E
-from paper_2207_00514_b200 import _lib
+"""Where the end-to-end call spends its time (developer tool): pageable numpy in, numpy out.
 
-pts = E.generate(E.DatasetSpec("blobs", 37_000_000, 3, seed=0))
-pinned = torch.from_numpy(pts).pin_memory().numpy()
+  python tools/e2e_breakdown.py [config]      (EMST_STAGE=0 for the plain cudaMemcpy path)
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2207_00514_b200 as E  # noqa: E402
+
+cfg = {"blobs3d_37m": ("blobs", 37_000_000, 3), "normal3d_10m": ("normal", 10_000_000, 3)}[
+    sys.argv[1] if len(sys.argv) > 1 else "blobs3d_37m"]
+pts = E.generate(E.DatasetSpec(cfg[0], cfg[1], cfg[2], seed=0))
 ctx = E.Context(0)
-for it in range(3):
+for it in range(4):
     t0 = time.perf_counter()
-    res = E.boruvka_emst(pinned, context=ctx)
+    res = E.boruvka_emst(pts, context=ctx)
     t1 = time.perf_counter()
-    s = float(np.sum(res.weights))
-    t2 = time.perf_counter()
-    print(f"call {1e3*(t1-t0):.1f} ms  np.sum {1e3*(t2-t1):.1f} ms  device total {1e3*res.phase_timings['mst']+1e3*res.phase_timings['tree']:.1f} ms")
-ne = len(pts) - 1
-e = torch.empty((ne, 2), dtype=torch.int64, pin_memory=True).numpy()
-w = torch.empty((ne,), dtype=torch.float64, pin_memory=True).numpy()
-st = _lib.Stats(); err = _lib.err_buf()
-for it in range(3):
-    t0 = time.perf_counter()
-    rc = _lib.load().emst_boruvka(ctx.handle, pinned.ctypes.data, len(pts), 3, _lib.SUBTREE_SKIP | _lib.UPPER_BOUNDS,
-                                  e.ctypes.data, w.ctypes.data, ctypes.byref(st), err, len(err))
-    t1 = time.perf_counter()
-    print(f"raw C call {1e3*(t1-t0):.1f} ms (phase total {st.phase_ms[7]:.1f} ms, h2d {st.h2d_bytes/1e6:.0f} MB d2h {st.d2h_bytes/1e6:.0f} MB)")
+    st = ctx.last_stats
+    dev = 1e3 * (res.phase_timings["tree"] + res.phase_timings["mst"])
+    print(f"stage={os.environ.get('EMST_STAGE', '1')} call {1e3 * (t1 - t0):.1f} ms, device tree+mst {dev:.1f} ms, "
+          f"host/PCIe {1e3 * (t1 - t0) - dev:.1f} ms (in {st.host_in_ms:.1f} ms, out {st.host_out_ms:.1f} ms)", flush=True)
