@@ -148,6 +148,19 @@ int emst_format_edges(const int64_t* edges, const double* weights, int64_t m, co
 int emst_format_points(const float* pts, int64_t n, int32_t d, const char** out, int64_t* len);
 void emst_text_free(void);
 
+/* The reference's CSV readers (data.py:148-198 read_points, 225-257 read_edges) on all host threads.
+ * emst_count_rows: lines of text[0, len) that are not blank (an upper bound of the rows).
+ * emst_parse_rows: parses text[start, len) -- its first line numbered line0 -- into rows [row0, cap):
+ * kind 0 edges "u,v,w" (out_a int64 (m, 2), out_b f64 (m)), kind 1 points (out_a f32 (n, width);
+ * width 0 = take 2 or 3 from the first non-blank line).  Plain ASCII spellings are converted here; the
+ * first line that is anything else (an error, or a spelling only Python's int()/float() take) stops the
+ * parse and is handed back for the caller to apply the reference's rules to it and resume after it.
+ * result[6] = {rows written in all, that line's number (-1: none), its begin, end (terminator
+ * excluded), the offset to resume at, the row width}. */
+int emst_count_rows(const char* text, int64_t len, int64_t* rows);
+int emst_parse_rows(const char* text, int64_t len, int64_t start, int64_t line0, int64_t row0, int32_t kind,
+                    int32_t width, void* out_a, void* out_b, int64_t cap, int64_t* result);
+
 /* compute_core_distances(build(points), points, k_pts) (metric.py:209-234): core_out n f64 (host), original
  * point order; k_pts in [1, n] (EMST_ERR_PARAM otherwise). */
 int emst_core_distances(emst_context* ctx, const float* pts, int64_t n, int32_t d, int32_t flags, int64_t k_pts,

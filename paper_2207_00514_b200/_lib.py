@@ -103,6 +103,8 @@ EXPORTS = (
     "emst_format_edges",
     "emst_format_points",
     "emst_text_free",
+    "emst_count_rows",
+    "emst_parse_rows",
     "emst_build_info",
 )
 
@@ -157,6 +159,8 @@ def load():
         L.emst_format_edges.argtypes = [vp, vp, i64, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64)]
         L.emst_format_points.argtypes = [vp, i64, i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(i64)]
         L.emst_text_free.argtypes = []
+        L.emst_count_rows.argtypes = [vp, i64, ctypes.POINTER(i64)]
+        L.emst_parse_rows.argtypes = [vp, i64, i64, i64, i64, i32, i32, vp, vp, i64, vp]
         for name in EXPORTS:
             getattr(L, name).restype = ctypes.c_int
         L.emst_build_info.restype = ctypes.c_char_p

@@ -22,6 +22,7 @@
 #include "radix_sort.cuh"
 #include "hostio.h"
 #include "textio.h"
+#include "textparse.h"
 #include "scan.cuh"
 
 using namespace emst;
@@ -967,6 +968,29 @@ int emst_format_points(const float* pts, int64_t n, int32_t d, const char** out,
   return EMST_OK;
 }
 void emst_text_free(void) { std::string().swap(g_text); }
+
+int emst_count_rows(const char* text, int64_t len, int64_t* rows) {
+  if (len < 0 || (len > 0 && !text) || !rows) return EMST_ERR_PARAM;
+  *rows = emst_io::count_rows(text, text + len);
+  return EMST_OK;
+}
+
+int emst_parse_rows(const char* text, int64_t len, int64_t start, int64_t line0, int64_t row0, int32_t kind,
+                    int32_t width, void* out_a, void* out_b, int64_t cap, int64_t* result) {
+  if (len < 0 || start < 0 || start > len || (len > 0 && !text) || !result || (kind != 0 && kind != 1)) return EMST_ERR_PARAM;
+  if (kind == 1 && width != 0 && width != 2 && width != 3) return EMST_ERR_PARAM;
+  if (!out_a || (kind == 0 && !out_b)) return EMST_ERR_PARAM;
+  const emst_io::ParseStop st =
+      emst_io::parse_csv(text, len, start, line0, row0, kind == 0, width, out_a, out_b, cap);
+  if (st.line == -2) return EMST_ERR_PARAM;   // outputs too small
+  result[0] = st.rows;
+  result[1] = st.line;
+  result[2] = st.begin;
+  result[3] = st.end;
+  result[4] = st.next;
+  result[5] = st.width;
+  return EMST_OK;
+}
 
 const char* emst_build_info(void) { return "emst_b200 sm_100a onesweep-lbvh-boruvka v1"; }
 

@@ -385,10 +385,60 @@ def make_api():
         json.dump({"cases": names}, fh, indent=1)
 
 
+IO_EDGE_CASES = [
+    "0,1,0.5\n1,2,0.25\n", "0,1,0.5\r\n1,2,0.25\r\n", "0,1,0.5\r1,2,0.25\r", "0,1,0.5", "", "\n \n\t\n",
+    "\n\n0,1,2\n  \n\x0c\n3,4,5\n\x1c\n", "  1 , 2 ,  0.5  \n", "+1,2,3\n", "1_0,2,3.5\n", "1,2,1e-400\n",
+    "1,2,1e400\n", "1,2,inf\n", "1,2,nan\n", "-1,2,3\n", "-0,2,3\n", "1,-2,3\n", "1,2\n", "1,2,3,4\n",
+    "a,2,3\n", "1,2,3.5e\n", "\u00a01,2,3\n", "\uff11,2,3\n", "1,2,.5\n1,2,5.\n1,2,-0.0\n1,2,1E+3\n",
+    "1,2,0x10\n", "1.0,2,3\n", "1,2,3\n\n5,6,bad\n7,8,9\n", "1,2,3\n4,5\n6,7,inf\n",
+    "007,08,1.25e-3\n", "1,2,3 4\n", "1,,3\n", ",1,2\n", "1,2,\n", "1,2,3\r\n\r\n4,5,6", "1 2,3,4\n",
+    "1,2,1e308\n3,4,2.2250738585072014e-308\n5,6,4.9e-324\n", "1,2,0.1000000000000000055511151231257827\n",
+]
+IO_POINT_CASES = [
+    "0.5,0.25\n1,2\n", "0.5,0.25,1\n1,2,3\n", "1\n", "1,2,3,4\n", "1,2\n3,4,5\n", "1,2,3\n4,5\n",
+    "1e39,2\n", "nan,1\n", "1,inf\n", "", "\n\n", "\n  \n1,2\n", "1_0,2\n", "a,b\n", "\u00a01,2\n",
+    "1,2\r\n3,4\r\n", "1,2\r3,4", ".5,5.\n-0,+1e-3\n", "1,2,\n", "1, 2 ,3\n", "3.4028235677973366e38,1\n",
+    "1e-50,1\n", "0.1,0.2,0.3\n0.4,0.5,bad\n",
+]
+
+
+def make_io():
+    """The reference's CSV readers on edge cases (line endings, whitespace, Python-only spellings, every
+    error): each input is written as UTF-8 to a file and read back through the reference's read_edges /
+    read_points (data.py:148-198, 225-257); the outputs or the exception (type and message) are recorded."""
+    import tempfile
+    emst = _import_reference()
+    out = {"edges": [], "points": []}
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "case.csv")
+        for kind, cases in (("edges", IO_EDGE_CASES), ("points", IO_POINT_CASES)):
+            for text in cases:
+                with open(path, "wb") as fh:
+                    fh.write(text.encode("utf-8"))
+                rec = {"text": text}
+                try:
+                    if kind == "edges":
+                        e, w = emst.read_edges(path)
+                        rec["edges"] = e.tolist()
+                        rec["weights_hex"] = [float(x).hex() for x in w]
+                    else:
+                        p = emst.read_points(path)
+                        rec["shape"] = list(p.shape)
+                        rec["points_hex"] = [float(x).hex() for x in p.reshape(-1)]
+                except Exception as exc:   # the reference's exception is part of the contract
+                    rec["error"] = type(exc).__name__
+                    rec["message"] = str(exc)
+                out[kind].append(rec)
+    with open(os.path.join(HERE, "io_cases.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 if __name__ == "__main__":
     which = sys.argv[1] if len(sys.argv) > 1 else "small"
     if which == "small":
         make_small()
+    elif which == "io":
+        make_io()
     elif which == "api":
         make_api()
     elif which == "mrd":

@@ -38,9 +38,19 @@ def test_library_is_built_for_sm100a():
     assert "sm_100a" in out
 
 
-def test_stats_struct_matches_header():
-    # emst_stats layout: field order and sizes must match the C struct
-    assert ctypes.sizeof(_lib.Stats) == 4 + 4 + 64 * 8 + 8 + 8 * 8 + 8 * 4 + 4 + 4 + 8 + 8 + 8 + 4 * 64 * 8 + 8
+def test_stats_struct_matches_header(tmp_path):
+    """emst_stats: every ctypes field sits at the C compiler's offset for include/emst_b200.h."""
+    import subprocess
+    names = [f[0] for f in _lib.Stats._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "emst_b200.h"\nint main(void) {\n'
+                   + "".join(f'  printf("%zu\\n", offsetof(emst_stats, {n}));\n' for n in names)
+                   + '  printf("%zu\\n", sizeof(emst_stats));\n  return 0;\n}\n')
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    want = [getattr(_lib.Stats, n).offset for n in names] + [ctypes.sizeof(_lib.Stats)]
+    assert got == want
 
 
 def test_exception_names_match_reference():

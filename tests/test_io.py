@@ -79,3 +79,64 @@ def test_io_errors(tmp_path):
     bad.write_bytes(b"XXXX" + bytes(20))
     with pytest.raises(E.ParseError):
         E.read_points(str(bad), fmt="bin")
+
+
+def _io_cases():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "io_cases.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("source", ["path", "textio"])
+def test_readers_match_reference_on_edge_cases(tmp_path, source):
+    """read_edges / read_points (native parser + the reference's per-line rules for the lines it hands back)
+    against the reference's own readers on line-ending, whitespace, Python-only spellings and every error
+    (tests/golden/make_goldens.py io)."""
+    cases = _io_cases()
+    for kind, reader in (("edges", E.read_edges), ("points", E.read_points)):
+        for i, rec in enumerate(cases[kind]):
+            path = tmp_path / f"{kind}{i}.csv"
+            path.write_bytes(rec["text"].encode("utf-8"))
+            src = str(path) if source == "path" else io.StringIO(rec["text"], newline=None)
+            if source == "textio":   # a text stream already applies universal newlines, like the reference's open()
+                src = io.StringIO(path.read_text())
+            if "error" in rec:
+                with pytest.raises(Exception) as info:
+                    reader(src)
+                assert type(info.value).__name__ == rec["error"], (kind, rec["text"])
+                assert str(info.value) == rec["message"], (kind, rec["text"])
+                continue
+            if kind == "edges":
+                e, w = reader(src)
+                assert e.dtype == np.int64 and e.shape == (len(rec["edges"]), 2), rec["text"]
+                assert e.tolist() == rec["edges"], rec["text"]
+                assert [float(x).hex() for x in w] == rec["weights_hex"], rec["text"]
+            else:
+                p = reader(src)
+                assert p.dtype == np.float32 and list(p.shape) == rec["shape"], rec["text"]
+                assert [float(x).hex() for x in p.reshape(-1)] == rec["points_hex"], rec["text"]
+
+
+def test_large_edge_file_reads_fast(tmp_path):
+    """37M-edge files are the use case; 2M edges here must take well under a second
+    of parsing, bit-exact through the %.17g round trip, with an error on the last line reported by number."""
+    import time
+    rng = np.random.default_rng(1)
+    m = 2_000_000
+    edges = np.stack([rng.integers(0, 2**31, m), rng.integers(0, 2**31, m)], 1).astype(np.int64)
+    w = rng.random(m) * np.exp(rng.normal(size=m) * 5)
+    path = tmp_path / "big.csv"
+    E.write_edges(str(path), edges, w)
+    t0 = time.perf_counter()
+    e2, w2 = E.read_edges(str(path))
+    dt = time.perf_counter() - t0
+    assert np.array_equal(e2, edges) and np.array_equal(w2, w)
+    assert dt < 5.0, dt
+    with open(path, "a") as fh:
+        fh.write("1,2,oops\n")
+    with pytest.raises(E.ParseError, match=f"line {m + 1}: could not parse '1,2,oops'"):
+        E.read_edges(str(path))
+    pts = E.generate(E.DatasetSpec("normal", 1_000_000, 3, seed=2))
+    E.write_points(str(tmp_path / "p.csv"), pts)
+    assert np.array_equal(E.read_points(str(tmp_path / "p.csv")), pts)
