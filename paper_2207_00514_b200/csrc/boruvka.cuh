@@ -502,8 +502,7 @@ struct MergeScanOp {
   const int* succ;
   const int* root;
   const EdgeKey* best;
-  unsigned long long* euv;
-  unsigned long long* ew;
+  EdgeKey* eout;   // emitted edges (u << 32 | v, weight bits), one 16-byte record each
   long long edge_base;
   int* newid;
   __device__ void load(long long i0, int cnt, unsigned long long* v) const {
@@ -529,9 +528,7 @@ struct MergeScanOp {
       const long long k = i0 + j;
       if (v[j] & 1ull) {
         const long long at = edge_base + (long long)(ex & 0x7fffffffull);
-        const EdgeKey e = best[k];
-        euv[at] = e.uv;
-        ew[at] = e.w;
+        eout[at] = best[k];
       }
       if (v[j] >> 31) newid[k] = (int)(ex >> 31);
       ex += v[j];
@@ -595,57 +592,104 @@ __global__ void k_fold_rows(unsigned long long* __restrict__ buf, int rows, long
 }
 
 // ------------------------------------------------------------ final output
+// The (w, u, v) order of the n - 1 edges (mst.py:745-747) in two steps:
+//   1. a stable 4-pass radix sort on a 32-bit key: the weight bits minus the
+//      smallest weight's bits, shifted right just enough to fit 32 bits
+//      (monotone in w >= 0: w_a < w_b implies key_a <= key_b; at 37M blobs 3D
+//      one key spans 2^24 f64 ulps, a relative 2^-28);
+//   2. every run of equal keys (true ties and the rare collisions) is put in
+//      exact (w bits, u << 32 | v) order -- 128-bit keys, all distinct.
+// Edges live as one 16-byte record (uv, w) so that every gather is one sector.
 constexpr int kThreadTie = 8;     // tie runs up to this long are ordered in registers by one thread
 constexpr int kShortTie = 32;     // ... up to this long by one warp each
 constexpr int kBlockTie = 4096;   // longer ones up to this long by one block each
 
-// One pass over the weight-sorted edges.  The thread at the start of each run
-// of equal weights measures it and puts it into (u, v) order (the uv keys are
-// distinct): a run of at most kThreadTie edges itself, in registers; a longer
-// one of at most kShortTie is listed in `mid` for a warp (k_edge_fix_mid), one
-// of at most kBlockTie in `runs` for a block (k_edge_fix_long), as (start,
-// length); a still longer run raises *max_run above kBlockTie and the host
-// switches to the two-key sort.
-__global__ void k_edge_ties(const unsigned long long* __restrict__ w, long long ne,
-                            const unsigned long long* __restrict__ euv, unsigned* __restrict__ order,
-                            unsigned* __restrict__ max_run, int2* __restrict__ runs, unsigned* __restrict__ run_count,
-                            int2* __restrict__ mid, unsigned* __restrict__ mid_count) {
+// range[0] = min, range[1] = max of the weight bits (range preset to (~0, 0))
+__global__ void __launch_bounds__(256) k_edge_wrange(const EdgeKey* __restrict__ e, long long ne,
+                                                     unsigned long long* __restrict__ range) {
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < ne; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long w = e[i].w;
+    lo = min(lo, w);
+    hi = max(hi, w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(range, lo);
+    atomicMax(range + 1, hi);
+  }
+}
+
+__device__ __forceinline__ int wkey_shift(const unsigned long long* range) {
+  const unsigned long long span = range[1] - range[0];
+  const int bits = span ? 64 - __clzll((long long)span) : 0;
+  return bits > 32 ? bits - 32 : 0;
+}
+
+// the 32-bit sort key of each emitted edge
+__global__ void k_edge_wkey(const EdgeKey* __restrict__ e, long long ne, const unsigned long long* __restrict__ range,
+                            unsigned* __restrict__ key) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < ne) key[i] = (unsigned)((e[i].w - range[0]) >> wkey_shift(range));
+}
+
+__device__ __forceinline__ bool wuv_less(const EdgeKey& a, const EdgeKey& b) {
+  return a.w < b.w || (a.w == b.w && a.uv < b.uv);
+}
+
+// One pass over the key-sorted edges.  The thread at the start of each run of
+// equal keys measures it and puts it into exact (w, u, v) order: a run of at
+// most kThreadTie edges itself, in registers; a longer one of at most kShortTie
+// is listed in `mid` for a warp (k_edge_fix_mid), one of at most kBlockTie in
+// `runs` for a block (k_edge_fix_long), as (start, length); a still longer run
+// raises *max_run above kBlockTie and the host redoes the order with the exact
+// two-key sort.
+__global__ void k_edge_ties(const unsigned* __restrict__ key, long long ne, const EdgeKey* __restrict__ eout,
+                            unsigned* __restrict__ order, unsigned* __restrict__ max_run, int2* __restrict__ runs,
+                            unsigned* __restrict__ run_count, int2* __restrict__ mid, unsigned* __restrict__ mid_count) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int len = 0;
   if (i + 1 < ne) {
-    const unsigned long long wi = w[i];
-    if (wi == w[i + 1] && (i == 0 || w[i - 1] != wi)) {   // a run starts here
+    const unsigned ki = key[i];
+    if (ki == key[i + 1] && (i == 0 || key[i - 1] != ki)) {   // a run starts here
       // run length by galloping + binary search (the keys are sorted), capped at kBlockTie + 1
       const long long cap = min(ne, i + kBlockTie + 1);   // positions [i, cap) may belong to the run
-      long long lo = i + 1, hi = i + 2;                   // w[lo] == wi; hi: first candidate to test
-      while (hi < cap && w[hi] == wi) {
+      long long lo = i + 1, hi = i + 2;                   // key[lo] == ki; hi: first candidate to test
+      while (hi < cap && key[hi] == ki) {
         lo = hi;
         hi = min(cap, i + 2 * (hi - i));
       }
       while (hi - lo > 1) {   // last equal position in [lo, hi)
         const long long m = (lo + hi) >> 1;
-        if (w[m] == wi) lo = m; else hi = m;
+        if (key[m] == ki) lo = m; else hi = m;
       }
       len = (int)(lo - i + 1);
     }
   }
   if (len == 2) {
     const unsigned o0 = order[i], o1 = order[i + 1];
-    if (euv[o0] > euv[o1]) { order[i] = o1; order[i + 1] = o0; }
+    if (wuv_less(eout[o1], eout[o0])) { order[i] = o1; order[i + 1] = o0; }
   } else if (len > 2 && len <= kThreadTie) {
     // in registers: all loads issued at once, then a fixed compare-exchange network
     unsigned o[kThreadTie];
-    unsigned long long k[kThreadTie];
+    EdgeKey k[kThreadTie];
 #pragma unroll
     for (int a = 0; a < kThreadTie; ++a) o[a] = a < len ? order[i + a] : 0u;
 #pragma unroll
-    for (int a = 0; a < kThreadTie; ++a) k[a] = a < len ? euv[o[a]] : ~0ull;
+    for (int a = 0; a < kThreadTie; ++a) {
+      if (a < len) k[a] = eout[o[a]];
+      else { k[a].w = ~0ull; k[a].uv = ~0ull; }
+    }
 #pragma unroll
     for (int a = 1; a < kThreadTie; ++a) {
 #pragma unroll
       for (int b = a; b > 0; --b) {
-        if (k[b - 1] > k[b]) {
-          const unsigned long long t = k[b - 1]; k[b - 1] = k[b]; k[b] = t;
+        if (wuv_less(k[b], k[b - 1])) {
+          const EdgeKey t = k[b - 1]; k[b - 1] = k[b]; k[b] = t;
           const unsigned u = o[b - 1]; o[b - 1] = o[b]; o[b] = u;
         }
       }
@@ -657,7 +701,7 @@ __global__ void k_edge_ties(const unsigned long long* __restrict__ w, long long 
   } else if (len > kShortTie) {
     runs[atomicAdd(run_count, 1u)] = make_int2((int)i, len);
   }
-  // runs of 3..kShortTie: one list append per warp
+  // runs of kThreadTie+1..kShortTie: one list append per warp
   const bool is_mid = len > kThreadTie && len <= kShortTie;
   const unsigned m = __ballot_sync(0xffffffffu, is_mid);
   if (m) {
@@ -670,97 +714,115 @@ __global__ void k_edge_ties(const unsigned long long* __restrict__ w, long long 
   }
 }
 
-// A warp per listed run of kThreadTie+1..kShortTie edges: bitonic sort of (uv, edge) across the lanes.
+// A warp per listed run of kThreadTie+1..kShortTie edges: bitonic sort of
+// ((w, uv), edge) across the lanes.  Grid-stride over the device-side count.
 __global__ void k_edge_fix_mid(const int2* __restrict__ mid, const unsigned* __restrict__ mid_count,
-                               const unsigned long long* __restrict__ euv, unsigned* __restrict__ order) {
+                               const EdgeKey* __restrict__ eout, unsigned* __restrict__ order) {
   const unsigned cnt = *mid_count;
   const int lane = (int)(threadIdx.x & 31u);
   const unsigned warps = gridDim.x * (blockDim.x >> 5);
   for (unsigned r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < cnt; r += warps) {
     const int2 run = mid[r];
     unsigned o = 0;
-    unsigned long long k = ~0ull;
+    EdgeKey k;
+    k.w = ~0ull;
+    k.uv = ~0ull;
     if (lane < run.y) {
       o = order[run.x + lane];
-      k = euv[o];
+      k = eout[o];
     }
 #pragma unroll
     for (int size = 2; size <= 32; size <<= 1) {
 #pragma unroll
       for (int j = size >> 1; j > 0; j >>= 1) {
-        const unsigned long long pk = __shfl_xor_sync(0xffffffffu, k, j);
+        EdgeKey p;
+        p.w = __shfl_xor_sync(0xffffffffu, k.w, j);
+        p.uv = __shfl_xor_sync(0xffffffffu, k.uv, j);
         const unsigned po = __shfl_xor_sync(0xffffffffu, o, j);
         const bool lower = (lane & j) == 0;
         const bool up = (lane & size) == 0;
         // the lower lane of a pair keeps the min when sorting up, the max otherwise
-        const bool take = lower == up ? pk < k : pk > k;
-        if (take) { k = pk; o = po; }
+        const bool take = lower == up ? wuv_less(p, k) : wuv_less(k, p);
+        if (take) { k = p; o = po; }
       }
     }
     if (lane < run.y) order[run.x + lane] = o;
   }
 }
 
-// One block per listed run (kShortTie < length <= kBlockTie): bitonic sort of
-// the run's (uv, edge) pairs in shared memory.
+// One block per listed run (kShortTie < length <= kBlockTie; grid-stride over
+// the device-side count): bitonic sort of the run's ((w, uv), edge) triples in
+// shared memory (dynamic, kEdgeFixSmem bytes).
+constexpr size_t kEdgeFixSmem = (size_t)kBlockTie * (16 + 4);
 __global__ void __launch_bounds__(1024) k_edge_fix_long(const int2* __restrict__ runs,
-                                                        const unsigned long long* __restrict__ euv,
+                                                        const unsigned* __restrict__ run_count,
+                                                        const EdgeKey* __restrict__ eout,
                                                         unsigned* __restrict__ order) {
-  __shared__ unsigned long long sk[kBlockTie];
-  __shared__ unsigned so[kBlockTie];
-  const int2 r = runs[blockIdx.x];
-  int size = 1;
-  while (size < r.y) size <<= 1;
-  for (int a = threadIdx.x; a < size; a += blockDim.x) {
-    const unsigned o = a < r.y ? order[r.x + a] : 0u;
-    so[a] = o;
-    sk[a] = a < r.y ? euv[o] : ~0ull;
-  }
-  __syncthreads();
-  for (int k = 2; k <= size; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int a = threadIdx.x; a < size; a += blockDim.x) {
-        const int b = a ^ j;
-        if (b > a) {
-          const bool up = (a & k) == 0;
-          const unsigned long long ka = sk[a], kb = sk[b];
-          if ((ka > kb) == up) {
-            sk[a] = kb; sk[b] = ka;
-            const unsigned t = so[a]; so[a] = so[b]; so[b] = t;
+  extern __shared__ __align__(16) unsigned char fix_smem[];
+  EdgeKey* sk = reinterpret_cast<EdgeKey*>(fix_smem);
+  unsigned* so = reinterpret_cast<unsigned*>(sk + kBlockTie);
+  const unsigned cnt = *run_count;
+  for (unsigned ri = blockIdx.x; ri < cnt; ri += gridDim.x) {
+    const int2 r = runs[ri];
+    int size = 1;
+    while (size < r.y) size <<= 1;
+    for (int a = threadIdx.x; a < size; a += blockDim.x) {
+      const unsigned o = a < r.y ? order[r.x + a] : 0u;
+      so[a] = o;
+      if (a < r.y) sk[a] = eout[o];
+      else { sk[a].w = ~0ull; sk[a].uv = ~0ull; }
+    }
+    __syncthreads();
+    for (int k = 2; k <= size; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int a = threadIdx.x; a < size; a += blockDim.x) {
+          const int b = a ^ j;
+          if (b > a) {
+            const bool up = (a & k) == 0;
+            const EdgeKey ka = sk[a], kb = sk[b];
+            if (wuv_less(kb, ka) == up) {
+              sk[a] = kb; sk[b] = ka;
+              const unsigned t = so[a]; so[a] = so[b]; so[b] = t;
+            }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
+    for (int a = threadIdx.x; a < r.y; a += blockDim.x) order[r.x + a] = so[a];
+    __syncthreads();   // (the shared arrays are reused by the next run)
   }
-  for (int a = threadIdx.x; a < r.y; a += blockDim.x) order[r.x + a] = so[a];
 }
 
-__global__ void k_edge_w_keys(const unsigned long long* __restrict__ ew, const unsigned* __restrict__ order, long long ne,
+// the exact fallback's keys: uv of each edge, then its weight bits in a given order
+__global__ void k_edge_uv_keys(const EdgeKey* __restrict__ eout, long long ne, unsigned long long* __restrict__ keys) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < ne) keys[i] = eout[i].uv;
+}
+__global__ void k_edge_w_keys(const EdgeKey* __restrict__ eout, const unsigned* __restrict__ order, long long ne,
                               unsigned long long* __restrict__ keys) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i < ne) keys[i] = ew[order[i]];
+  if (i < ne) keys[i] = eout[order[i]].w;
 }
 
-// sorted weight bits + edge order -> the reference's int64 (u, v) rows and f64 weights
-__global__ void k_edge_emit(const unsigned long long* __restrict__ w, const unsigned* __restrict__ order,
-                            const unsigned long long* __restrict__ euv, long long ne, long long* __restrict__ edges,
-                            double* __restrict__ weights) {
+// edge order -> the reference's int64 (u, v) rows and f64 weights
+__global__ void k_edge_emit(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout, long long ne,
+                            long long* __restrict__ edges, double* __restrict__ weights) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= ne) return;
-  const unsigned long long uv = euv[order[i]];
-  reinterpret_cast<longlong2*>(edges)[i] = make_longlong2((long long)(uv >> 32), (long long)(uv & 0xffffffffull));
-  weights[i] = __longlong_as_double((long long)w[i]);
+  const EdgeKey e = eout[order[i]];
+  reinterpret_cast<longlong2*>(edges)[i] = make_longlong2((long long)(e.uv >> 32), (long long)(e.uv & 0xffffffffull));
+  weights[i] = __longlong_as_double((long long)e.w);
 }
 
 // the host-pointer entry's variant: packed (u << 32 | v) rows, 8 bytes per edge over PCIe (hostio.h)
-__global__ void k_edge_emit_packed(const unsigned long long* __restrict__ w, const unsigned* __restrict__ order,
-                                   const unsigned long long* __restrict__ euv, long long ne,
+__global__ void k_edge_emit_packed(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout, long long ne,
                                    unsigned long long* __restrict__ packed, double* __restrict__ weights) {
   long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (i >= ne) return;
-  packed[i] = euv[order[i]];
-  weights[i] = __longlong_as_double((long long)w[i]);
+  const EdgeKey e = eout[order[i]];
+  packed[i] = e.uv;
+  weights[i] = __longlong_as_double((long long)e.w);
 }
 
 // ----------------------------------------------------- total weight (numpy order)

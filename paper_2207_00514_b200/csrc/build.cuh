@@ -174,7 +174,8 @@ constexpr int kGatherPer = 4;
 template <int D>
 __global__ void __launch_bounds__(kGatherThreads)
 k_gather(const float* __restrict__ pts, long long n, const unsigned* __restrict__ sorted_idx,
-         unsigned* __restrict__ perm, float4* __restrict__ spts, unsigned* __restrict__ iperm) {
+         unsigned* __restrict__ perm, float4* __restrict__ spts, unsigned* __restrict__ iperm,
+         const Scene* __restrict__ scene, unsigned long long* __restrict__ codes) {
   const long long base = (long long)blockIdx.x * (kGatherThreads * kGatherPer) + threadIdx.x;
   unsigned p[kGatherPer];
   float4 v[kGatherPer];
@@ -200,6 +201,17 @@ k_gather(const float* __restrict__ pts, long long n, const unsigned* __restrict_
       spts[s] = v[j];
       perm[s] = p[j];
       if (iperm) iperm[p[j]] = (unsigned)s;
+      // the sorted Morton codes, recomputed from the gathered point (the sort's
+      // last pass writes only the permutation): k_morton's formula, bit for bit
+      if (codes) {
+        if (D == 3)
+          codes[s] = (spread_bits3(lattice_cell(v[j].x, scene->lo[0], scene->inv[0], 2097152.0)) << 2) |
+                     (spread_bits3(lattice_cell(v[j].y, scene->lo[1], scene->inv[1], 2097152.0)) << 1) |
+                     spread_bits3(lattice_cell(v[j].z, scene->lo[2], scene->inv[2], 2097152.0));
+        else
+          codes[s] = (spread_bits2(lattice_cell(v[j].x, scene->lo[0], scene->inv[0], 2147483648.0)) << 1) |
+                     spread_bits2(lattice_cell(v[j].y, scene->lo[1], scene->inv[1], 2147483648.0));
+      }
     }
   }
 }

@@ -169,8 +169,7 @@ struct emst_context {
   DevBuf<unsigned long long> ub;
   DevBuf<EdgeKey> best, shard_keys;
   DevBuf<int> succ, ptr, root, newid, fin;
-  DevBuf<unsigned long long> euv;   // emitted edges: u << 32 | v
-  DevBuf<unsigned long long> ew;
+  DevBuf<EdgeKey> eout;   // emitted edges: (u << 32 | v, weight bits)
   DevBuf<unsigned long long> xw, xuv;   // multi-GPU exchange
   DevBuf<unsigned long long> scan_scratch;
   DevBuf<long long> counters;   // [0] evals, [1] scan total, [2] err, [3] overflow
@@ -197,7 +196,6 @@ struct emst_context {
   int dim = 0;
   long long n = 0;
   bool tree_valid = false;
-  bool sort_attr_done = false;
 };
 
 namespace {
@@ -272,47 +270,103 @@ __global__ void k_iota_u32(unsigned* a, long long n) {
   if (i < n) a[i] = (unsigned)i;
 }
 
-// Stable sort of (keys, vals) by the low `bits` key bits.  `iota` means vals is
-// the identity permutation (not read; generated in the first pass).  keys_alt /
-// vals_alt are the ping-pong partners; *keys_res / *vals_res receive whichever
-// pair holds the result.
-void radix_sort(emst_context* c, long long n, int bits, unsigned long long* keys, unsigned* vals, bool iota,
-                unsigned long long* keys_alt, unsigned* vals_alt, unsigned long long** keys_res, unsigned** vals_res) {
-  const int passes = (bits + kRadixBits - 1) / kRadixBits;
+template <class K, int O, bool I>
+void sort_pass(emst_context* c, long long n, const K* kin, const unsigned* vin, void* kout, unsigned* vout, int shift,
+               int p, int slot) {
+  auto kern = k_onesweep<K, O, I>;
+  const size_t smem = sizeof(SortSmemT<K>);
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   // (host-side, cheap)
+  const long long tiles = sort_tiles(n);
+  CK(cudaMemsetAsync(c->sort_status.p, 0, (size_t)tiles * kRadix * sizeof(unsigned), c->stream));
+  launch(c, kern, (unsigned)tiles, kSortThreads, smem, kin, vin,
+         reinterpret_cast<typename SortOutKey<K, O>::type*>(kout), vout, n, shift,
+         (const unsigned*)(c->sort_off.p + p * kRadix), c->sort_status.p, c->sort_misc.p + 1 + slot);
+}
+
+template <class K, int O>
+void sort_pass_v(emst_context* c, long long n, const K* kin, const unsigned* vin, bool iota, void* kout,
+                 unsigned* vout, int shift, int p, int slot) {
+  if (iota) sort_pass<K, O, true>(c, n, kin, nullptr, kout, vout, shift, p, slot);
+  else sort_pass<K, O, false>(c, n, kin, vin, kout, vout, shift, p, slot);
+}
+
+// Histograms of the first `passes` 8-bit digits of n keys and their exclusive
+// offsets; bit p of sort_misc[0] is set when digit p varies (a pass over it is
+// not the identity).  No host sync.
+template <class K>
+void sort_prepare(emst_context* c, long long n, int passes, const K* keys) {
   c->sort_hist.ensure(kMaxPasses * kRadix);
   c->sort_off.ensure(kMaxPasses * kRadix);
   c->sort_misc.ensure(16);
-  const long long tiles = sort_tiles(n);
-  c->sort_status.ensure((size_t)tiles * kRadix);
+  c->sort_status.ensure((size_t)sort_tiles(n) * kRadix);
   CK(cudaMemsetAsync(c->sort_hist.p, 0, kMaxPasses * kRadix * sizeof(unsigned), c->stream));
   CK(cudaMemsetAsync(c->sort_misc.p, 0, 16 * sizeof(unsigned), c->stream));
-  launch(c, k_digit_histograms, (unsigned)std::min<long long>(grid_for(n, kSortThreads), (long long)c->num_sms * 4),
-         kSortThreads, 0, (const unsigned long long*)keys, n, passes, c->sort_hist.p);
+  launch(c, k_digit_histograms<K>, (unsigned)std::min<long long>(grid_for(n, kSortThreads), (long long)c->num_sms * 4),
+         kSortThreads, 0, keys, n, passes, c->sort_hist.p);
   launch(c, k_digit_offsets, (unsigned)passes, kRadix, 0, (const unsigned*)c->sort_hist.p, n, c->sort_off.p,
          c->sort_misc.p);
+}
+
+// Stable LSD sort of u64 keys with the identity as values, over the digits set
+// in `active` (from sort_prepare): the permutation only (bvh.py:317 -- the
+// sorted keys are not written back; k_gather recomputes them).  While the low
+// digits are sorted the whole key travels; once only digits >= 4 remain, only
+// its high 32 bits do, and the last pass writes just the values (24 -> 16 -> 8
+// bytes per key written).  Ping-pongs between k0/k1 and v0/v1; returns the buffer
+// holding the permutation.
+unsigned* sort_permutation(emst_context* c, long long n, unsigned long long* keys, unsigned active) {
+  std::vector<int> act;
+  for (int p = 0; p < kMaxPasses; ++p)
+    if (active & (1u << p)) act.push_back(p);
+  if (act.empty()) {   // every digit constant: the identity
+    launch(c, k_iota_u32, grid_for(n, 256), 256, 0, c->v0.p, n);
+    return c->v0.p;
+  }
+  void* kin = const_cast<unsigned long long*>(keys);
+  void* kout = (void*)keys == (void*)c->k0.p ? (void*)c->k1.p : (void*)c->k0.p;
+  unsigned *vin = c->v0.p, *vout = c->v1.p;
+  bool wide = true, iota = true;
+  for (size_t i = 0; i < act.size(); ++i) {
+    const int p = act[i];
+    const bool last = i + 1 == act.size();
+    const int out = last ? kOutNone : (wide && act[i + 1] >= 4) ? kOutHigh32 : kOutSame;
+    if (wide) {
+      const auto* k = reinterpret_cast<const unsigned long long*>(kin);
+      if (out == kOutNone) sort_pass_v<unsigned long long, kOutNone>(c, n, k, vin, iota, kout, vout, p * 8, p, (int)i);
+      else if (out == kOutHigh32) sort_pass_v<unsigned long long, kOutHigh32>(c, n, k, vin, iota, kout, vout, p * 8, p, (int)i);
+      else sort_pass_v<unsigned long long, kOutSame>(c, n, k, vin, iota, kout, vout, p * 8, p, (int)i);
+    } else {
+      const auto* k = reinterpret_cast<const unsigned*>(kin);
+      if (out == kOutNone) sort_pass_v<unsigned, kOutNone>(c, n, k, vin, iota, kout, vout, p * 8 - 32, p, (int)i);
+      else sort_pass_v<unsigned, kOutSame>(c, n, k, vin, iota, kout, vout, p * 8 - 32, p, (int)i);
+    }
+    if (out == kOutHigh32) wide = false;
+    iota = false;
+    // the next pass reads what this one wrote; its input (the codes, at first) is free
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  return vin;
+}
+
+// Stable sort of (keys, vals) by the low `bits` key bits (general u64 form:
+// the building blocks and the final order's long-tie fallback).  `iota` means
+// vals is the identity permutation (not read; generated in the first pass).
+// keys_alt / vals_alt are the ping-pong partners; *keys_res / *vals_res receive
+// whichever pair holds the result.  Reads the active-digit mask back (a sync).
+void radix_sort(emst_context* c, long long n, int bits, unsigned long long* keys, unsigned* vals, bool iota,
+                unsigned long long* keys_alt, unsigned* vals_alt, unsigned long long** keys_res, unsigned** vals_res) {
+  const int passes = (bits + kRadixBits - 1) / kRadixBits;
+  sort_prepare<unsigned long long>(c, n, passes, keys);
   unsigned active = 0;
   CK(cudaMemcpyAsync(&active, c->sort_misc.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  const size_t smem = sizeof(SortSmem);
-  if (!c->sort_attr_done) {
-    CK(cudaFuncSetAttribute(k_onesweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(k_onesweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    c->sort_attr_done = true;
-  }
   unsigned long long *kin = keys, *kout = keys_alt;
   unsigned *vin = vals, *vout = vals_alt;
   int launched = 0;
   for (int p = 0; p < passes; ++p) {
     if (!(active & (1u << p))) continue;
-    CK(cudaMemsetAsync(c->sort_status.p, 0, (size_t)tiles * kRadix * sizeof(unsigned), c->stream));
-    if (iota)
-      launch(c, k_onesweep<true>, (unsigned)tiles, kSortThreads, smem, (const unsigned long long*)kin,
-             (const unsigned*)nullptr, kout, vout, n, p * kRadixBits, (const unsigned*)(c->sort_off.p + p * kRadix),
-             c->sort_status.p, c->sort_misc.p + 1 + launched);
-    else
-      launch(c, k_onesweep<false>, (unsigned)tiles, kSortThreads, smem, (const unsigned long long*)kin,
-             (const unsigned*)vin, kout, vout, n, p * kRadixBits, (const unsigned*)(c->sort_off.p + p * kRadix),
-             c->sort_status.p, c->sort_misc.p + 1 + launched);
+    sort_pass_v<unsigned long long, kOutSame>(c, n, kin, vin, iota, kout, vout, p * kRadixBits, p, launched);
     iota = false;
     std::swap(kin, kout);
     std::swap(vin, vout);
@@ -365,9 +419,13 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
     launch(c, k_scene<2>, sg, kSceneThreads, 0, dev_pts, n, c->part_lo.p, c->part_hi.p, c->part_bad.p, c->scene.p);
   if (d == 3) launch(c, k_morton<3>, grid_for(n, 256), 256, 0, dev_pts, n, (const Scene*)c->scene.p, c->k0.p);
   else launch(c, k_morton<2>, grid_for(n, 256), 256, 0, dev_pts, n, (const Scene*)c->scene.p, c->k0.p);
-  // the scene check needs the host anyway before anything data-dependent
+  // digit histograms of the codes; the scene check needs the host anyway, so the
+  // mask of varying digits comes back with it (the build's one sync)
+  sort_prepare<unsigned long long>(c, n, kMaxPasses, c->k0.p);
   Scene sc;
+  unsigned active = 0;
   CK(cudaMemcpyAsync(&sc, c->scene.p, sizeof(Scene), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaMemcpyAsync(&active, c->sort_misc.p, sizeof(unsigned), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   if (sc.bad_row != 0x7fffffffffffffffll) {
     Failure f;
@@ -375,17 +433,20 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
     snprintf(f.msg, sizeof(f.msg), "point %lld has a non-finite coordinate", sc.bad_row);
     throw f;
   }
-  unsigned long long* skeys;
-  unsigned* svals;
-  radix_sort(c, n, d == 3 ? 63 : 62, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &skeys, &svals);
-  // sorted codes -> k-buffer `skeys`, permutation -> `svals`
+  unsigned* svals = sort_permutation(c, n, c->k0.p, active);
+  // slot-order points, perm / iperm, and the sorted codes (recomputed) into k0
+  unsigned long long* skeys = c->k0.p;
   {
     const unsigned g = grid_for(n, kGatherThreads * kGatherPer);
     // the inverse permutation: in the gather for small n, else by parts of <= kIpermPart targets
     const int parts = c->iperm_parts > 0 ? c->iperm_parts : (int)((n + kIpermPart - 1) / kIpermPart);
     unsigned* ip = parts <= 1 ? c->iperm.p : nullptr;
-    if (d == 3) launch(c, k_gather<3>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, ip);
-    else launch(c, k_gather<2>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, ip);
+    if (d == 3)
+      launch(c, k_gather<3>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, ip,
+             (const Scene*)c->scene.p, skeys);
+    else
+      launch(c, k_gather<2>, g, kGatherThreads, 0, dev_pts, n, (const unsigned*)svals, c->perm.p, c->spts.p, ip,
+             (const Scene*)c->scene.p, skeys);
     if (!ip) {
       for (int k = 0; k < parts; ++k) {
         const unsigned lo = (unsigned)(k * n / parts), hi = (unsigned)((k + 1) * n / parts);
@@ -456,8 +517,7 @@ void ensure_rounds(emst_context* c, long long n) {
   c->root.ensure(n);
   c->newid.ensure(n);
   c->fin.ensure(n);
-  c->euv.ensure(n);
-  c->ew.ensure(n);
+  c->eout.ensure(n);
 }
 
 __global__ void k_iota_int(int* a, long long n) {
@@ -681,7 +741,7 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
          (const unsigned*)c->iperm.p, c->succ.p, err, singletons);
   launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
   launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, c->root.p, err);
-  run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->euv.p, c->ew.p, edge_base, c->newid.p},
+  run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->eout.p, edge_base, c->newid.p},
            true);
   launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->root.p, (const int*)c->newid.p, comps, c->fin.p);
   launch(c, k_relabel, grid_for((n + 3) / 4, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
@@ -695,56 +755,77 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
   return (long long)(tot >> 31);
 }
 
-// Final order (w, u, v) of the n - 1 edges (mst.py:745-747).  One stable radix
-// sort on the weight bits (passes whose digit is constant are skipped); equal
-// weights are then put in (u, v) order: runs of up to kShortTie edges by the
-// thread at the run start, anything longer by the exact two-key LSD sort.
+// Final order (w, u, v) of the n - 1 edges (mst.py:745-747): a 4-pass stable
+// radix sort on the f32-rounded weight (16 bytes per edge per pass instead of
+// 24 over 8 passes on the f64 bits), then every run of equal keys put in exact
+// (w, u, v) order (k_edge_ties and the warp / block fix-ups, which take their
+// run counts from the device: no host sync).  A run longer than kBlockTie
+// (checked by the caller at the solve's final counter read, sort_overflowed)
+// is redone by sort_and_emit_exact.
+void emit_edges(emst_context* c, const unsigned* order, long long ne, long long* edges_dst, double* w_dst, bool packed) {
+  if (packed)
+    launch(c, k_edge_emit_packed, grid_for(ne, 256), 256, 0, order, (const EdgeKey*)c->eout.p, ne,
+           reinterpret_cast<unsigned long long*>(edges_dst), w_dst);
+  else
+    launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, order, (const EdgeKey*)c->eout.p, ne, edges_dst, w_dst);
+}
+
 void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* w_dst, bool packed = false) {
   if (ne <= 0) return;
-  unsigned long long* keys;
-  unsigned* order;
-  CK(cudaMemcpyAsync(c->k0.p, c->ew.p, ne * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c->stream));
-  radix_sort(c, ne, 64, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
+  unsigned* key = reinterpret_cast<unsigned*>(c->k0.p);
+  c->sort_misc.ensure(16);
+  // (min, max) of the weight bits in words 12..15 of sort_misc (reset by sort_prepare after use)
+  unsigned long long* wr = reinterpret_cast<unsigned long long*>(c->sort_misc.p + 12);
+  CK(cudaMemsetAsync(wr, 0xff, sizeof(unsigned long long), c->stream));
+  CK(cudaMemsetAsync(wr + 1, 0, sizeof(unsigned long long), c->stream));
+  launch(c, k_edge_wrange, (unsigned)std::min<long long>(grid_for(ne, 256), (long long)c->num_sms * 8), 256, 0,
+         (const EdgeKey*)c->eout.p, ne, wr);
+  launch(c, k_edge_wkey, grid_for(ne, 256), 256, 0, (const EdgeKey*)c->eout.p, ne, (const unsigned long long*)wr, key);
+  sort_prepare<unsigned>(c, ne, 4, key);
+  unsigned* kin = key;
+  unsigned* kout = reinterpret_cast<unsigned*>(c->k1.p);
+  unsigned *vin = c->v0.p, *vout = c->v1.p;
+  for (int p = 0; p < 4; ++p) {
+    sort_pass_v<unsigned, kOutSame>(c, ne, kin, vin, p == 0, kout, vout, p * 8, p, p);
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  unsigned* order = vin;
   long long* tie = dev_counter(c, 7);   // low word: longest run, high word: listed long runs
   CK(cudaMemsetAsync(tie, 0, sizeof(long long), c->stream));
   c->tie_runs.ensure(ne / (kShortTie + 1) + 1);
   unsigned* mid_n = reinterpret_cast<unsigned*>(dev_counter(c, 11));
   CK(cudaMemsetAsync(mid_n, 0, sizeof(long long), c->stream));
-  c->tie_mid.ensure(ne / 3 + 1);
-  launch(c, k_edge_ties, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, ne,
-         (const unsigned long long*)c->euv.p, order, (unsigned*)tie, c->tie_runs.p, (unsigned*)tie + 1, c->tie_mid.p,
-         mid_n);
-  read_counters(c);
-  const unsigned max_run = (unsigned)(c->host_counters[7] & 0xffffffffll);
-  const unsigned long_runs = (unsigned)((unsigned long long)c->host_counters[7] >> 32);
-  if (max_run > (unsigned)kBlockTie) {
-    // a very long tie run: exact two-key sort -- stable by (u, v), then stable by w
-    CK(cudaMemcpyAsync(c->k0.p, c->euv.p, ne * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, c->stream));
-    radix_sort(c, ne, 64, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
-    unsigned long long* kin = keys == c->k0.p ? c->k1.p : c->k0.p;
-    unsigned* vin_alt = order == c->v1.p ? c->v0.p : c->v1.p;
-    launch(c, k_edge_w_keys, grid_for(ne, 256), 256, 0, (const unsigned long long*)c->ew.p, (const unsigned*)order, ne, kin);
-    unsigned long long* keys2;
-    unsigned* order2;
-    radix_sort(c, ne, 64, kin, order, false, keys, vin_alt, &keys2, &order2);
-    keys = keys2;
-    order = order2;
-  } else {
-    const unsigned mids = (unsigned)(c->host_counters[11] & 0xffffffffll);
-    if (mids)   // a warp per run
-      launch(c, k_edge_fix_mid, (mids + 7) / 8, 256, 0, (const int2*)c->tie_mid.p, (const unsigned*)mid_n,
-             (const unsigned long long*)c->euv.p, order);
-  }
-  if (max_run <= (unsigned)kBlockTie && long_runs) {
-    launch(c, k_edge_fix_long, long_runs, 1024, 0, (const int2*)c->tie_runs.p, (const unsigned long long*)c->euv.p,
-           order);
-  }
-  if (packed)
-    launch(c, k_edge_emit_packed, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, (const unsigned*)order,
-           (const unsigned long long*)c->euv.p, ne, reinterpret_cast<unsigned long long*>(edges_dst), w_dst);
-  else
-    launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, (const unsigned long long*)keys, (const unsigned*)order,
-           (const unsigned long long*)c->euv.p, ne, edges_dst, w_dst);
+  c->tie_mid.ensure(ne / (kThreadTie + 1) + 1);
+  launch(c, k_edge_ties, grid_for(ne, 256), 256, 0, (const unsigned*)kin, ne, (const EdgeKey*)c->eout.p, order,
+         (unsigned*)tie, c->tie_runs.p, (unsigned*)tie + 1, c->tie_mid.p, mid_n);
+  // (grids sized for the worst case; the kernels stride over the device-side counts)
+  launch(c, k_edge_fix_mid, (unsigned)c->num_sms * 8, 256, 0, (const int2*)c->tie_mid.p, (const unsigned*)mid_n,
+         (const EdgeKey*)c->eout.p, order);
+  CK(cudaFuncSetAttribute(k_edge_fix_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEdgeFixSmem));
+  launch(c, k_edge_fix_long, (unsigned)c->num_sms, 1024, kEdgeFixSmem, (const int2*)c->tie_runs.p,
+         (const unsigned*)tie + 1, (const EdgeKey*)c->eout.p, order);
+  emit_edges(c, order, ne, edges_dst, w_dst, packed);
+}
+
+// true when sort_and_emit met a tie run longer than kBlockTie (after a counter read)
+bool sort_overflowed(emst_context* c) { return (unsigned)(c->host_counters[7] & 0xffffffffll) > (unsigned)kBlockTie; }
+
+// The exact two-key order for inputs with very long runs of equal weights: a
+// stable sort by (u << 32 | v), then a stable sort by the weight bits.
+void sort_and_emit_exact(emst_context* c, long long ne, long long* edges_dst, double* w_dst, bool packed = false) {
+  if (ne <= 0) return;
+  unsigned long long* keys;
+  unsigned* order;
+  launch(c, k_edge_uv_keys, grid_for(ne, 256), 256, 0, (const EdgeKey*)c->eout.p, ne, c->k0.p);
+  radix_sort(c, ne, 64, c->k0.p, c->v0.p, true, c->k1.p, c->v1.p, &keys, &order);
+  unsigned long long* kin = keys == c->k0.p ? c->k1.p : c->k0.p;
+  unsigned* vin_alt = order == c->v1.p ? c->v0.p : c->v1.p;
+  launch(c, k_edge_w_keys, grid_for(ne, 256), 256, 0, (const EdgeKey*)c->eout.p, (const unsigned*)order, ne, kin);
+  unsigned long long* keys2;
+  unsigned* order2;
+  radix_sort(c, ne, 64, kin, order, false, keys, vin_alt, &keys2, &order2);
+  emit_edges(c, order2, ne, edges_dst, w_dst, packed);
 }
 
 // float(np.sum(weights)) on the device in numpy's summation order.
@@ -827,6 +908,24 @@ void prepare_cores(emst_context* c, long long n, long long k_pts, const double* 
   c->core = c->core_slot.p;
 }
 
+#ifdef EMST_VISIT_HIST
+void visit_hist_reset(emst_context* c) {
+  const int2* r = c->range.p;
+  CK(cudaMemcpyToSymbolAsync(g_visit_range, &r, sizeof(r), 0, cudaMemcpyHostToDevice, c->stream));
+  static const unsigned long long zero[2][32] = {};
+  CK(cudaMemcpyToSymbolAsync(g_visit_hist, zero, sizeof(zero), 0, cudaMemcpyHostToDevice, c->stream));
+}
+void visit_hist_print(emst_context* c) {
+  unsigned long long h[2][32];
+  CK(cudaMemcpyFromSymbol(h, g_visit_hist, sizeof(h)));
+  for (int k = 0; k < 2; ++k) {
+    fprintf(stderr, "[emst] visits (%s) by log2 range:", k ? "pop" : "climb");
+    for (int b = 0; b < 32; ++b) if (h[k][b]) fprintf(stderr, " %d:%llu", b, h[k][b]);
+    fprintf(stderr, "\n");
+  }
+}
+#endif
+
 void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags, long long* edges_dev,
            double* w_dev, emst_stats* st, long long k_pts = 1, const double* core_host = nullptr, bool packed = false) {
   cudaEvent_t t0, t1, t2, t3;
@@ -839,6 +938,9 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   CK(cudaEventRecord(t0, c->stream));
   build_tree(c, dev_pts, n, d);
   CK(cudaEventRecord(t3, c->stream));
+#ifdef EMST_VISIT_HIST
+  visit_hist_reset(c);
+#endif
   CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
   prepare_cores(c, n, k_pts, core_host);   // (mutual reachability; the "core" phase)
   CK(cudaEventRecord(t1, c->stream));
@@ -910,6 +1012,13 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   CK(cudaEventRecord(t2, c->stream));
   CK(cudaEventSynchronize(t2));
   read_counters(c);
+  if (sort_overflowed(c)) {   // a run of > kBlockTie equal f32 weight keys: the exact two-key order
+    sort_and_emit_exact(c, edges, edges_dev, w_dev, packed);
+    total_weight(c, w_dev, edges, st);
+    CK(cudaEventRecord(t2, c->stream));
+    CK(cudaEventSynchronize(t2));
+    read_counters(c);
+  }
   long long evals = c->host_counters[0];
   if (c->world > 1) {
     // total work counter over ranks (instrumentation only)
@@ -918,6 +1027,9 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     evals = c->host_counters[0];
   }
   st->leaf_distance_evals = evals;
+#ifdef EMST_VISIT_HIST
+  if (c->trace) visit_hist_print(c);
+#endif
   float ms_tree = 0, ms_mst = 0;
   float ms_core = 0;
   CK(cudaEventElapsedTime(&ms_tree, t0, t3));
@@ -1060,7 +1172,7 @@ int emst_context_destroy(emst_context* c) {
   c->label.release(); c->bprefix.release(); c->big_tops.release(); c->top.release();
   c->front[0].release(); c->front[1].release(); c->core_slot.release(); c->core_tmp.release(); c->nfn_lb.release(); c->qlist.release(); c->ub.release(); c->best.release(); c->shard_keys.release();
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
-  c->euv.release(); c->ew.release(); c->xw.release(); c->xuv.release(); c->exch_host.release();
+  c->eout.release(); c->xw.release(); c->xuv.release(); c->exch_host.release();
   c->stager.release();
   c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release(); c->tie_mid.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
@@ -1650,12 +1762,11 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
     launch(c, k_cluster_min, grid_for(s, 256), 256, 0, (const int*)c->root.p, (const long long*)dreps.p, s, cmin.p);
     std::vector<int> ptr(s), newlab(n);
     std::vector<long long> cm(s);
-    std::vector<unsigned long long> euv(emitted), ew(emitted);
+    std::vector<EdgeKey> eo(emitted);
     CK(cudaMemcpyAsync(ptr.data(), c->root.p, s * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(cm.data(), cmin.p, s * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     if (emitted) {
-      CK(cudaMemcpyAsync(euv.data(), c->euv.p, emitted * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
-      CK(cudaMemcpyAsync(ew.data(), c->ew.p, emitted * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaMemcpyAsync(eo.data(), c->eout.p, emitted * sizeof(EdgeKey), cudaMemcpyDeviceToHost, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
     for (long long i = 0; i < n; ++i) {
@@ -1667,9 +1778,9 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
       if (ptr[k] == (int)k) new_reps[nn++] = cm[k];
     std::sort(new_reps, new_reps + nn);
     for (long long e = 0; e < emitted; ++e) {
-      out_u[e] = (long long)(euv[e] >> 32);
-      out_v[e] = (long long)(euv[e] & 0xffffffffull);
-      memcpy(&out_w[e], &ew[e], 8);
+      out_u[e] = (long long)(eo[e].uv >> 32);
+      out_v[e] = (long long)(eo[e].uv & 0xffffffffull);
+      memcpy(&out_w[e], &eo[e].w, 8);
     }
     *n_edges = emitted;
     *n_new = nn;

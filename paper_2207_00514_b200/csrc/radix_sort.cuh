@@ -35,13 +35,14 @@ constexpr unsigned kSortFlagAgg = 1u << 30;
 constexpr unsigned kSortFlagPrefix = 2u << 30;
 constexpr unsigned kSortValueMask = (1u << 30) - 1;
 
+template <class K>
 __global__ void __launch_bounds__(kSortThreads)
-k_digit_histograms(const unsigned long long* __restrict__ keys, long long n, int passes, unsigned* __restrict__ hist) {
+k_digit_histograms(const K* __restrict__ keys, long long n, int passes, unsigned* __restrict__ hist) {
   __shared__ unsigned s_hist[kMaxPasses][kRadix];
   for (int i = threadIdx.x; i < kMaxPasses * kRadix; i += blockDim.x) (&s_hist[0][0])[i] = 0;
   __syncthreads();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    unsigned long long k = keys[i];
+    const unsigned long long k = keys[i];
     for (int p = 0; p < passes; ++p) atomicAdd(&s_hist[p][(k >> (p * kRadixBits)) & (kRadix - 1)], 1u);
   }
   __syncthreads();
@@ -72,14 +73,16 @@ __global__ void k_digit_offsets(const unsigned* __restrict__ hist, long long n, 
   if (t == 0 && !s_trivial) atomicOr(active_mask, 1u << p);
 }
 
-struct SortSmem {
-  unsigned long long keys[kSortTile];
+template <class K>
+struct SortSmemT {
+  K keys[kSortTile];
   unsigned vals[kSortTile];
   unsigned short whist[kSortWarps][kRadix];   // per-warp digit counts, then exclusive warp offsets
   unsigned tile_excl[kRadix];
   unsigned long long global_base[kRadix];
   long long tile;
 };
+using SortSmem = SortSmemT<unsigned long long>;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -100,7 +103,14 @@ __device__ __forceinline__ unsigned warp_incl_sum_u32(unsigned v) {
 #define EMST_SORT_MINB 4
 #endif
 
-// One counting-sort pass over `shift`'s 8-bit digit.  Per tile of 4096 keys:
+// What a pass writes besides the values: the keys as they are, only their high
+// 32 bits (the passes left read nothing below them), or nothing (last pass).
+enum SortOut { kOutSame = 0, kOutHigh32 = 1, kOutNone = 2 };
+template <class K, int O> struct SortOutKey { using type = K; };
+template <class K> struct SortOutKey<K, kOutHigh32> { using type = unsigned; };
+template <class K> struct SortOutKey<K, kOutNone> { using type = unsigned; };
+
+// One counting-sort pass over `shift`'s 8-bit digit of K keys.  Per tile of kSortTile keys:
 //   1. warp-private stable ranks: the lanes holding the same digit are found
 //      with 8 ballots (one per digit bit); the lowest bumps the warp's counter
 //      in shared memory by the group size and broadcasts the old value (items
@@ -111,47 +121,59 @@ __device__ __forceinline__ unsigned warp_incl_sum_u32(unsigned v) {
 //      are only read here, so the ranking holds just the keys and packed ranks)
 //      -- this is the work that overlaps the predecessors' progress --
 //   4. decoupled look-back for each digit's global start, then the tile is
-//      written out digit-run-contiguous.
-template <bool kIotaValues>
+//      written out digit-run-contiguous (keys converted as SortOut says).
+template <class K, int kOut, bool kIotaValues>
 __global__ void __launch_bounds__(kSortThreads, EMST_SORT_MINB)
-k_onesweep(const unsigned long long* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
-           unsigned long long* __restrict__ keys_out, unsigned* __restrict__ vals_out, long long n, int shift,
-           const unsigned* __restrict__ digit_offset, unsigned* __restrict__ status, unsigned* __restrict__ ticket) {
+k_onesweep(const K* __restrict__ keys_in, const unsigned* __restrict__ vals_in,
+           typename SortOutKey<K, kOut>::type* __restrict__ keys_out, unsigned* __restrict__ vals_out, long long n,
+           int shift, const unsigned* __restrict__ digit_offset, unsigned* __restrict__ status,
+           unsigned* __restrict__ ticket) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  SortSmem& sm = *reinterpret_cast<SortSmem*>(smem_raw);
+  SortSmemT<K>& sm = *reinterpret_cast<SortSmemT<K>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // peer-mask bins of the ranking, two sets per warp (alternating items), in the
+  // key staging area, which is only written after the ranking
+  static_assert(sizeof(SortSmemT<K>::keys) >= 2 * kSortWarps * kRadix * sizeof(unsigned), "match bins");
+  unsigned* const mbin = reinterpret_cast<unsigned*>(sm.keys);
   if (tid == 0) sm.tile = (long long)atomicAdd(ticket, 1u);
   for (int i = tid; i < kSortWarps * kRadix / 2; i += kSortThreads) reinterpret_cast<unsigned*>(&sm.whist[0][0])[i] = 0u;
+  for (int i = tid; i < 2 * kSortWarps * kRadix; i += kSortThreads) mbin[i] = 0u;
   __syncthreads();
   const long long tile = sm.tile;
   const long long base = tile * kSortTile;
   const long long warp_base = base + warp * (32 * kSortItems);
 
-  unsigned long long key[kSortItems];
+  K key[kSortItems];
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
     const long long i = warp_base + j * 32 + lane;
-    key[j] = i < n ? keys_in[i] : ~0ull;
+    key[j] = i < n ? keys_in[i] : (K)~(K)0;
   }
   const unsigned lt = lanemask_lt();
   unsigned rank2[kSortItems / 2];   // two 16-bit ranks per register
 #pragma unroll
   for (int j = 0; j < kSortItems; ++j) {
+    // Stable warp-local rank: every lane ORs its bit into its digit's peer mask,
+    // the lowest lane of each digit group bumps the warp's counter by the group
+    // size, and a lane's rank is the counter's old value plus its lower peers
+    // (items are visited in input order, so equal digits keep their order).
+    // The mask is cleared by its leader; the next item uses the other bin set,
+    // so the clear never races with the next ORs.
     const long long i = warp_base + j * 32 + lane;
     const bool ok = i < n;
     const unsigned d = (unsigned)((key[j] >> shift) & (kRadix - 1));
-    unsigned peers = __ballot_sync(0xffffffffu, ok);
-#pragma unroll
-    for (int b = 0; b < kRadixBits; ++b) {
-      const unsigned bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-      peers &= ((d >> b) & 1u) ? bal : ~bal;
-    }
+    unsigned* bin = mbin + ((j & 1) * kSortWarps + warp) * kRadix + d;
+    if (ok) atomicOr(bin, 1u << lane);
+    __syncwarp();
+    const unsigned peers = ok ? *reinterpret_cast<volatile unsigned*>(bin) : 0u;
     const int leader = __ffs(peers) - 1;   // (an invalid lane has peers = 0: leader -1)
     unsigned before = 0;
     if (ok && lane == leader) {
       before = sm.whist[warp][d];
       sm.whist[warp][d] = (unsigned short)(before + __popc(peers));
     }
+    __syncwarp();   // (every lane has read its mask and the counters are updated)
+    if (ok && lane == leader) *bin = 0u;
     before = __shfl_sync(0xffffffffu, before, leader < 0 ? 0 : leader);
     const unsigned r = before + __popc(peers & lt);
     if (j & 1) rank2[j >> 1] |= r << 16; else rank2[j >> 1] = r;
@@ -220,10 +242,11 @@ k_onesweep(const unsigned long long* __restrict__ keys_in, const unsigned* __res
   const long long remain = n - base;
   const int count = remain < kSortTile ? (int)remain : kSortTile;
   for (int i = tid; i < count; i += kSortThreads) {
-    const unsigned long long k = sm.keys[i];
+    const K k = sm.keys[i];
     const unsigned d = (unsigned)((k >> shift) & (kRadix - 1));
     const unsigned long long dst = sm.global_base[d] + (unsigned)(i - sm.tile_excl[d]);
-    keys_out[dst] = k;
+    if (kOut == kOutSame) keys_out[dst] = (typename SortOutKey<K, kOut>::type)k;
+    else if (kOut == kOutHigh32) keys_out[dst] = (unsigned)((unsigned long long)k >> 32);
     vals_out[dst] = sm.vals[i];
   }
 }

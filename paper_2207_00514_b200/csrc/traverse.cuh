@@ -27,6 +27,13 @@
 
 namespace emst {
 
+#ifdef EMST_VISIT_HIST
+// developer instrumentation (EXTRA_NVFLAGS=-DEMST_VISIT_HIST, printed under EMST_TRACE):
+// node visits by log2 of the node's slot-range size, climb steps [0] and pops [1]
+__device__ unsigned long long g_visit_hist[2][32];
+__device__ const int2* g_visit_range;
+#endif
+
 template <int D>
 __device__ __forceinline__ void child_box(const Node3& rec, int side, float* lo, float* hi) {
   if (side == 0) {
@@ -575,6 +582,12 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     }
     if (node >= 0) {
       ++visits;
+#ifdef EMST_VISIT_HIST
+      {
+        const int2 rg = g_visit_range[node];
+        atomicAdd(&g_visit_hist[climbing ? 0 : 1][31 - __clz(rg.y - rg.x + 1)], 1ull);
+      }
+#endif
       const auto rec = load_node(nodes + node);
       int2 u = make_int2(-1, 0);
       if (climbing) u = __ldg(up + node);   // (parent link, prefix length of `climb`)

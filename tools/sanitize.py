@@ -36,7 +36,7 @@ for kind, n, d in cases:
     print(f"ok {kind} {d}D n={n}", flush=True)
 pts = E.generate(E.DatasetSpec("blobs", 3000, 3, seed=2))
 got = E.boruvka_emst(pts, "mrd", 4)
-want = orc.boruvka_emst(pts, "mrd", 4)
+want = orc.boruvka_emst(pts, k_pts=4)
 assert np.array_equal(got.edges, want.edges) and np.array_equal(got.weights, want.weights), "mrd"
 # ties: coincident points and a grid
 grid = np.stack(np.meshgrid(np.arange(40), np.arange(40)), -1).reshape(-1, 2).astype(np.float32)
