@@ -365,24 +365,34 @@ def test_host_transfer_paths(large_golden, env, monkeypatch):
         ctx.close()
 
 
+def _sort_key32(w):
+    """The 32-bit key k_edge_wkey sorts on: weight bits minus the smallest, shifted to fit 32 bits."""
+    b = w.view(np.uint64)
+    span = int(b.max() - b.min())
+    shift = max(0, span.bit_length() - 32)
+    return (b - b.min()) >> np.uint64(shift)
+
+
 @pytest.mark.parametrize("d", [2, 3])
 @pytest.mark.parametrize("jitter", [0.5, 3.0, 30.0])
-def test_f32_key_collisions_order_exactly(d, jitter):
-    """The final order sorts on the weight rounded to f32, then puts every run of equal keys in exact
-    (w, u, v) order.  A lattice of spacing 2^16 with uniform jitter has its edge lengths in a narrow
-    band around 65536 where one f32 value spans 2^-7: runs of equal keys hold distinct f64 weights,
-    ~3 to ~60 per run depending on the jitter (the thread, warp and block fix-ups).  The oracle
-    restatement is the checker."""
+def test_equal_sort_keys_order_exactly(d, jitter):
+    """The final order sorts on a 32-bit key (weight bits minus the smallest, shifted right to fit), then
+    puts every run of equal keys in exact (w, u, v) order.  A jittered lattice of spacing 2^16 has its
+    edge lengths in a narrow band around 65536; one far outlier (1e18) stretches the weight range so
+    that one key spans ~2^26 f64 ulps: runs of equal keys then hold distinct weights, ~2 to ~60 per
+    run depending on the jitter (the thread, warp and block fix-ups).  The oracle restatement is the
+    checker."""
     from oracle import oracle as orc
     rng = np.random.default_rng(11 + d)
     side = 28 if d == 3 else 150
     g = np.arange(side, dtype=np.float64) * 65536
     lat = np.stack(np.meshgrid(*([g] * d), indexing="ij"), -1).reshape(-1, d)
     pts = (lat + rng.uniform(-jitter, jitter, lat.shape)).astype(np.float32)
+    pts = np.concatenate([pts, np.full((1, d), 1e18, np.float32)])
     res = E.boruvka_emst(pts)
     ref = orc.boruvka_emst(pts)
-    keys = res.weights.astype(np.float32)
-    inside = (np.diff(keys) == 0) & (np.diff(res.weights) != 0)
+    keys = _sort_key32(ref.weights)
+    inside = (np.diff(keys) == 0) & (np.diff(ref.weights) != 0)
     assert np.count_nonzero(inside) > 100   # runs of equal keys with distinct weights do occur
     assert np.array_equal(res.edges, ref.edges) and np.array_equal(res.weights, ref.weights)
     assert res.total_weight == ref.total_weight
