@@ -336,69 +336,139 @@ __device__ __forceinline__ void put_node_boxes(Node2* nodes, int node, const flo
 #endif
 constexpr int kRefitThreads = EMST_REFIT_THREADS;
 
-// Bottom-up boxes, one thread per leaf, in two phases.  A block owns the
-// kRefitThreads consecutive slots [B, B+T); a node whose slot range lies inside
-// it (Karras: then its index is in [B, B+T) too) has all its leaves in this
-// block, so its arrivals are counted in shared memory and the first arrival
-// parks its box there: no global atomics or fences, and the second arrival
-// writes the node's two child boxes with three 16-byte stores.  The first node
-// that straddles the block edge, and every ancestor of it, uses the global
-// protocol: child box into the record, acq_rel arrival count, the second
-// arrival reads both boxes back from L2.
+// Bottom-up boxes in two kernels.  k_refit: a block owns the kRefitThreads
+// consecutive slots [B, E) and the internal nodes of the same indices.  A node
+// whose slot range lies inside the block (Karras: its index is then in [B, E)
+// too) gets both child boxes at once from a sparse table of the block's points
+// in shared memory (level l holds the box of slots [t, t + 2^l)); any range is
+// the union of two overlapping power-of-two windows.  No arrival protocol, no
+// divergence, no dependent global reads.  The roots of the block's subtrees
+// (a leaf or an inside node whose parent straddles the block edge) put their
+// box into the parent's record and count an acq_rel arrival; the second
+// arrival lists the parent for k_refit_up, which climbs the upper tree.
+constexpr int kRefitLevels = 9;   // 2^8 = kRefitThreads: a node can span the whole block
+template <int D>
+constexpr size_t refit_smem() { return (size_t)kRefitLevels * kRefitThreads * 6 * sizeof(float); }
+
+// table layout [level][coordinate][slot] (lo 0..D-1, hi D..2D-1): conflict-free per coordinate
+__device__ __forceinline__ int refit_at(int l, int k, int t) { return (l * 6 + k) * kRefitThreads + t; }
+
+template <int D>
+__device__ __forceinline__ void refit_query(const float* tab, int a, int b, float* lo, float* hi) {
+  // box of block-relative slots [a, b] (inclusive)
+  const int len = b - a + 1;
+  const int l = 31 - __clz(len);
+  const int y = b - (1 << l) + 1;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    lo[k] = fminf(tab[refit_at(l, k, a)], tab[refit_at(l, k, y)]);
+    hi[k] = fmaxf(tab[refit_at(l, D + k, a)], tab[refit_at(l, D + k, y)]);
+  }
+#pragma unroll
+  for (int k = D; k < 3; ++k) { lo[k] = 0.f; hi[k] = 0.f; }
+}
+
 template <class Node>
+__device__ __forceinline__ void refit_escape(Node* nodes, int link, const float* lo, const float* hi,
+                                             unsigned* __restrict__ arrivals, int* __restrict__ up_list,
+                                             unsigned* __restrict__ up_count) {
+  const int node = link >> 1;
+  put_child_box(nodes, node, link & 1, lo, hi);
+  // relaxed: nothing in this launch reads the boxes; k_refit_up (the next
+  // launch) sees them all
+  if (atomicAdd(&arrivals[node], 1u) != 0) up_list[atomicAdd(up_count, 1u)] = node;
+}
+
+template <class Node, int D>
 __global__ void __launch_bounds__(kRefitThreads)
 k_refit(const float4* __restrict__ spts, long long n, Node* nodes, const int2* __restrict__ range,
         const int* __restrict__ node_parent, const int* __restrict__ leaf_parent, unsigned* __restrict__ arrivals,
-        Box3* __restrict__ root_box) {
-  __shared__ unsigned s_arr[kRefitThreads];
-  __shared__ float s_box[kRefitThreads][2][6];
+        Box3* __restrict__ root_box, int* __restrict__ up_list, unsigned* __restrict__ up_count) {
+  extern __shared__ __align__(16) float tab[];   // [level][slot][lo D, hi D]
+  __shared__ int2 s_range[kRefitThreads];
+  const int t = threadIdx.x;
   const long long B = (long long)blockIdx.x * kRefitThreads;
-  s_arr[threadIdx.x] = 0;
-  __syncthreads();
-  const long long s = B + threadIdx.x;
-  if (s >= n) return;
-  const long long E = min(B + kRefitThreads, n);   // block's slots: [B, E)
-  const float4 p = spts[s];
-  float lo[3] = {p.x, p.y, p.z}, hi[3] = {p.x, p.y, p.z};
-  int link = leaf_parent[s];
-  for (;;) {
-    const int node = link >> 1, side = link & 1;
-    const int2 r = range[node];
-    if (r.x < B || r.y >= E) break;
-    float* mine = s_box[node - B][side];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { mine[k] = lo[k]; mine[3 + k] = hi[k]; }
-    __threadfence_block();
-    if (atomicAdd(&s_arr[node - B], 1u) == 0) return;
-    __threadfence_block();
-    const float* other = s_box[node - B][side ^ 1];
-    float olo[3], ohi[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { olo[k] = other[k]; ohi[k] = other[3 + k]; }
-    if (side == 0) put_node_boxes(nodes, node, lo, hi, olo, ohi);
-    else put_node_boxes(nodes, node, olo, ohi, lo, hi);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { lo[k] = fminf(lo[k], olo[k]); hi[k] = fmaxf(hi[k], ohi[k]); }
-    if (node == 0) {
-      for (int k = 0; k < 3; ++k) { root_box->lo[k] = lo[k]; root_box->hi[k] = hi[k]; }
-      return;
-    }
-    link = node_parent[node];
+  const int cnt = (int)min((long long)kRefitThreads, n - B);
+  const long long i = B + t;   // this thread's slot and internal node
+  float4 p = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (t < cnt) {
+    p = spts[i];
+    tab[refit_at(0, 0, t)] = p.x; tab[refit_at(0, 1, t)] = p.y;
+    tab[refit_at(0, D, t)] = p.x; tab[refit_at(0, D + 1, t)] = p.y;
+    if (D == 3) { tab[refit_at(0, 2, t)] = p.z; tab[refit_at(0, 5, t)] = p.z; }
   }
-  for (;;) {
-    const int node = link >> 1, side = link & 1;
-    put_child_box(nodes, node, side, lo, hi);
-    // acq_rel: the first arrival's box is released by its increment and the
-    // second arrival acquires it with its own (no full fences needed)
-    unsigned prev;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&arrivals[node]) : "memory");
-    if (prev == 0) return;   // first arrival: sibling not done yet
-    get_union_box(nodes, node, lo, hi);
-    if (node == 0) {
-      for (int k = 0; k < 3; ++k) { root_box->lo[k] = lo[k]; root_box->hi[k] = hi[k]; }
-      return;
+  s_range[t] = i < n - 1 ? range[i] : make_int2(-1, -1);
+  __syncthreads();
+  for (int l = 1; l < kRefitLevels && (1 << l) <= cnt; ++l) {
+    const int h = 1 << (l - 1);
+    if (t + (1 << l) <= cnt) {
+#pragma unroll
+      for (int k = 0; k < D; ++k) {
+        tab[refit_at(l, k, t)] = fminf(tab[refit_at(l - 1, k, t)], tab[refit_at(l - 1, k, t + h)]);
+        tab[refit_at(l, D + k, t)] = fmaxf(tab[refit_at(l - 1, D + k, t)], tab[refit_at(l - 1, D + k, t + h)]);
+      }
     }
-    link = node_parent[node];
+    __syncthreads();
+  }
+  const long long E = B + cnt;
+  auto inside = [&](int node) -> bool {
+    if (node < B || node >= E) return false;
+    const int2 r = s_range[node - B];
+    return r.x >= B && r.y < E;
+  };
+  if (i < n - 1) {
+    const int2 r = s_range[t];
+    if (r.x >= B && r.y < E) {
+      const int lref = nodes[i].ref.x;
+      const int gamma = lref >= 0 ? lref : ~lref;
+      float alo[3], ahi[3], blo[3], bhi[3];
+      refit_query<D>(tab, r.x - (int)B, gamma - (int)B, alo, ahi);
+      refit_query<D>(tab, gamma + 1 - (int)B, r.y - (int)B, blo, bhi);
+      put_node_boxes(nodes, (int)i, alo, ahi, blo, bhi);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { alo[k] = fminf(alo[k], blo[k]); ahi[k] = fmaxf(ahi[k], bhi[k]); }
+      if (i == 0) {
+        for (int k = 0; k < 3; ++k) { root_box->lo[k] = alo[k]; root_box->hi[k] = ahi[k]; }
+      } else {
+        const int link = node_parent[i];
+        if (!inside(link >> 1)) refit_escape(nodes, link, alo, ahi, arrivals, up_list, up_count);
+      }
+    }
+  }
+  if (t < cnt) {
+    const int link = leaf_parent[i];
+    if (!inside(link >> 1)) {
+      const float lo[3] = {p.x, p.y, D == 3 ? p.z : 0.f};
+      refit_escape(nodes, link, lo, lo, arrivals, up_list, up_count);
+    }
+  }
+}
+
+// The upper tree: one thread per node listed by k_refit (both children done),
+// climbing with the acq_rel arrival protocol until it arrives first.
+template <class Node>
+__global__ void __launch_bounds__(256)
+k_refit_up(Node* nodes, const int* __restrict__ node_parent, unsigned* __restrict__ arrivals,
+           const int* __restrict__ up_list, const unsigned* __restrict__ up_count, Box3* __restrict__ root_box) {
+  const unsigned cnt = *up_count;
+  for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < cnt; t += gridDim.x * blockDim.x) {
+    int node = up_list[t];
+    float lo[3], hi[3];
+    for (;;) {
+      get_union_box(nodes, node, lo, hi);
+      if (node == 0) {
+        for (int k = 0; k < 3; ++k) { root_box->lo[k] = lo[k]; root_box->hi[k] = hi[k]; }
+        break;
+      }
+      const int link = node_parent[node];
+      node = link >> 1;
+      put_child_box(nodes, node, link & 1, lo, hi);
+      // acq_rel: the first arrival's box is released by its increment and the
+      // second arrival acquires it with its own (no full fences needed)
+      unsigned prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&arrivals[node]) : "memory");
+      if (prev == 0) break;   // first arrival: sibling not done yet
+    }
   }
 }
 

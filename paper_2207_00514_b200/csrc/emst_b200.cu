@@ -103,7 +103,7 @@ constexpr long long kIpermPart = 1ll << 23;   // inverse-permutation targets per
 constexpr int kCounters = 16;   // [0] evals [1] scan total [2] err [3] overflow [4] work [5] visits
                                 // [6] found [7] ties [8] frontier size [9] skipped queries [10] big tops [11] mid tie runs
                                 // [12] slots of component 1 (last round) [13] the component left out
-                                // [14] slots listed by the prefilter
+                                // [14] slots listed by the prefilter [15] refit nodes for the upper tree
 
 struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
@@ -457,20 +457,30 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
   if (n > 1) {
     const long long m = n - 1;
     CK(cudaMemsetAsync(c->arrivals.p, 0, m * sizeof(unsigned), c->stream));
+    unsigned* up_n = reinterpret_cast<unsigned*>(dev_counter(c, 15));
+    CK(cudaMemsetAsync(up_n, 0, sizeof(long long), c->stream));
+    int* up_list = reinterpret_cast<int*>(c->v0.p);   // (the sort's value buffer is free after the gather)
+    const unsigned up_grid = (unsigned)c->num_sms * 8;
     if (d == 3) {
       Node3* nodes = reinterpret_cast<Node3*>(c->nodes.p);
       launch(c, k_karras<Node3>, grid_for(m, 256), 256, 0, (const unsigned long long*)skeys, n, nodes, c->range.p,
              c->node_parent.p, c->leaf_parent.p, c->node_delta.p);
-      launch(c, k_refit<Node3>, grid_for(n, kRefitThreads), kRefitThreads, 0, (const float4*)c->spts.p, n, nodes,
+      CK(cudaFuncSetAttribute(k_refit<Node3, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)refit_smem<3>()));
+      launch(c, k_refit<Node3, 3>, grid_for(n, kRefitThreads), kRefitThreads, refit_smem<3>(), (const float4*)c->spts.p, n, nodes,
              (const int2*)c->range.p,
-             (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p);
+             (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p, up_list, up_n);
+      launch(c, k_refit_up<Node3>, up_grid, 256, 0, nodes, (const int*)c->node_parent.p, c->arrivals.p,
+             (const int*)up_list, (const unsigned*)up_n, c->root_box.p);
     } else {
       Node2* nodes = reinterpret_cast<Node2*>(c->nodes.p);
       launch(c, k_karras<Node2>, grid_for(m, 256), 256, 0, (const unsigned long long*)skeys, n, nodes, c->range.p,
              c->node_parent.p, c->leaf_parent.p, c->node_delta.p);
-      launch(c, k_refit<Node2>, grid_for(n, kRefitThreads), kRefitThreads, 0, (const float4*)c->spts.p, n, nodes,
+      CK(cudaFuncSetAttribute(k_refit<Node2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)refit_smem<2>()));
+      launch(c, k_refit<Node2, 2>, grid_for(n, kRefitThreads), kRefitThreads, refit_smem<2>(), (const float4*)c->spts.p, n, nodes,
              (const int2*)c->range.p,
-             (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p);
+             (const int*)c->node_parent.p, (const int*)c->leaf_parent.p, c->arrivals.p, c->root_box.p, up_list, up_n);
+      launch(c, k_refit_up<Node2>, up_grid, 256, 0, nodes, (const int*)c->node_parent.p, c->arrivals.p,
+             (const int*)up_list, (const unsigned*)up_n, c->root_box.p);
     }
   }
   if (n > 1)
