@@ -210,6 +210,19 @@ int emst_merge_components(emst_context* ctx, int64_t n, const int64_t* reps, int
                           int64_t* out_v, double* out_w, int64_t* n_edges, int64_t* new_reps, int64_t* n_new,
                           char* err, size_t errlen);
 
+/* Device-resident building blocks (mst.py:436-547 called round by round without host copies):
+ *  - emst_tree_token: names the tree the context holds (0: none); it changes with every build
+ *    (emst_build, a solve, or a building block that had to build);
+ *  - emst_context_reuse_tree: the next building-block call on this context skips its own
+ *    build when `token` still names the context's tree (same points, n and d: the caller's
+ *    promise, as the reference's Bvh is a snapshot of its points) -- one call only;
+ *  - emst_context_set_state_on_device: while on, the state arrays the four building blocks
+ *    take and return (labels, internal labels, bounds, best edges, reps, merged edges, new reps)
+ *    are device pointers on the context's device; the points stay host (or the reused tree). */
+int emst_tree_token(emst_context* ctx, int64_t* token);
+int emst_context_reuse_tree(emst_context* ctx, int64_t token);
+int emst_context_set_state_on_device(emst_context* ctx, int on);
+
 /* Library identification: compiled arch string (e.g. "sm_100a") and a build tag. */
 const char* emst_build_info(void);
 

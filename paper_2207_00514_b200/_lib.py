@@ -90,6 +90,9 @@ EXPORTS = (
     "emst_context_set_virtual_shards",
     "emst_context_set_exchange",
     "emst_context_wait_stream",
+    "emst_tree_token",
+    "emst_context_reuse_tree",
+    "emst_context_set_state_on_device",
     "emst_boruvka",
     "emst_boruvka_mrd",
     "emst_core_distances",
@@ -146,6 +149,9 @@ def load():
         L.emst_context_set_stream.argtypes = [vp, vp]
         L.emst_context_set_exchange.argtypes = [vp, EXCHANGE_FN, vp]
         L.emst_context_wait_stream.argtypes = [vp, vp]
+        L.emst_tree_token.argtypes = [vp, ctypes.POINTER(i64)]
+        L.emst_context_reuse_tree.argtypes = [vp, i64]
+        L.emst_context_set_state_on_device.argtypes = [vp, ctypes.c_int]
         L.emst_boruvka.argtypes = [vp, vp, i64, i32, i32, vp, vp, ctypes.POINTER(Stats), cp, sz]
         L.emst_boruvka_mrd.argtypes = [vp, vp, i64, i32, i32, i64, vp, vp, vp, ctypes.POINTER(Stats), cp, sz]
         L.emst_core_distances.argtypes = [vp, vp, i64, i32, i32, i64, vp, cp, sz]
@@ -240,6 +246,20 @@ class Context:
         if tensor.device.index != self.device:
             raise InvalidParameterError(f"tensor on cuda:{tensor.device.index} given to a cuda:{self.device} context")
         self.wait_stream(torch.cuda.current_stream(tensor.device))
+
+    def tree_token(self) -> int:
+        """Names the tree this context holds now (0: none); every build changes it."""
+        t = ctypes.c_int64(0)
+        raise_for(load().emst_tree_token(self.handle, ctypes.byref(t)), None)
+        return int(t.value)
+
+    def reuse_tree(self, token: int) -> None:
+        """The next building-block call skips its build if `token` still names this context's tree."""
+        raise_for(load().emst_context_reuse_tree(self.handle, int(token)), None)
+
+    def state_on_device(self, on: bool) -> None:
+        """While on, the building blocks take and return device pointers for the round state."""
+        raise_for(load().emst_context_set_state_on_device(self.handle, 1 if on else 0), None)
 
     def set_stream(self, stream) -> None:
         """Run on an external CUDA stream (a torch.cuda.Stream or a raw cudaStream_t int; None = own)."""

@@ -51,6 +51,10 @@ class Bvh:
     sweep_starts: np.ndarray | None = None
     # the points the GPU built this tree from (the building blocks rebuild from them)
     points: np.ndarray | None = field(default=None, repr=False, compare=False)
+    # the native context that still holds this tree on the device, and the token naming it there:
+    # the building blocks reuse it instead of rebuilding while the token is current
+    tree_context: object = field(default=None, repr=False, compare=False)
+    tree_token: int = field(default=0, repr=False, compare=False)
 
     @property
     def num_internal(self) -> int:
@@ -206,8 +210,10 @@ def build(points) -> Bvh:
                                     ctypes.byref(n_starts), e, len(e))
     _lib.raise_for(rc, e)
     host = keep if isinstance(keep, np.ndarray) else keep.detach().cpu().numpy()
+    token = ctx.tree_token()
+    ctx.tree_points = (token, points, host)   # (compute_upper_bounds names points, not a Bvh)
     return Bvh(n, d, perm, left[:m], right[:m], parent[:m], leaf_parent, box_lo[:m], box_hi[:m], order[:m],
-               starts[:n_starts.value].copy(), host)
+               starts[:n_starts.value].copy(), host, ctx, token)
 
 
 def _ref_bound(bvh: Bvh, coords: np.ndarray, q: np.ndarray, ref: int) -> float:

@@ -196,6 +196,18 @@ struct emst_context {
   int dim = 0;
   long long n = 0;
   bool tree_valid = false;
+  long long tree_token = 0;       // bumped by every build: names the tree the context holds
+  long long reuse_token = 0;      // set by emst_context_reuse_tree: the next building block may skip its build
+  bool state_on_device = false;   // building-block arrays are device pointers (emst_context_set_state_on_device)
+  // find_component_outgoing_edges keeps its nearest-foreign proofs for the next call on the
+  // same tree when that call's components coarsen these (foreign sets only shrink then)
+  DevBuf<float> bb_nfn;           // the proofs (slot order)
+  DevBuf<int> bb_prev;            // the labels they were proved under
+  DevBuf<unsigned> ident;         // identity permutation (the merge building block: point order is slot order)
+  long long ident_n = 0;
+  long long bb_token = 0;         // tree they belong to (0: none)
+  double bb_skip = 0.0;           // share of the last call's queries settled up front
+  int bb_calls = 0;               // calls so far in the chain of coarsening calls (the solve's round - 1)
 };
 
 namespace {
@@ -487,6 +499,7 @@ void build_tree(emst_context* c, const float* dev_pts, long long n, int d) {
     launch(c, k_pack_up, grid_for(n - 1, 256), 256, 0, (const int*)c->node_parent.p, (const int*)c->node_delta.p, n - 1,
            c->up.p);
   c->tree_valid = true;
+  c->tree_token++;
 }
 
 const float* stage_points(emst_context* c, const float* pts, long long n, int d, int flags, emst_stats* st) {
@@ -744,11 +757,11 @@ void round_find_all(emst_context* c, long long n, long long comps, int flags) {
 // Returns the new component count (and the edges emitted via *emitted).
 // singletons: the solve's round 1, where label[s] == s
 long long round_merge(emst_context* c, long long n, long long comps, long long edge_base, long long* emitted,
-                      double* ms_merge = nullptr, bool singletons = false) {
+                      double* ms_merge = nullptr, bool singletons = false, const unsigned* iperm = nullptr) {
   cudaEvent_t m0 = timer_event(c);
   int* err = reinterpret_cast<int*>(dev_counter(c, 2));
   launch(c, k_merge_succ, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, (const int*)c->label.p,
-         (const unsigned*)c->iperm.p, c->succ.p, err, singletons);
+         iperm ? iperm : (const unsigned*)c->iperm.p, c->succ.p, err, singletons);
   launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
   launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, c->root.p, err);
   run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->eout.p, edge_base, c->newid.p},
@@ -961,6 +974,7 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   CK(cudaMemsetAsync(c->top.p, 0, n * sizeof(int), c->stream));
   c->front_n = -1;
   c->skip_frac = 0.0;
+  c->bb_token = 0;   // (the solve reuses the round buffers)
   long long comps = n, edges = 0;
   const int max_it = max_iterations(n);
   st->component_counts[0] = n;
@@ -1177,6 +1191,7 @@ int emst_context_destroy(emst_context* c) {
   c->pts.release(); c->scene.release(); c->part_lo.release(); c->part_hi.release(); c->part_bad.release();
   c->k0.release(); c->k1.release(); c->v0.release(); c->v1.release();
   c->sort_hist.release(); c->sort_off.release(); c->sort_status.release(); c->sort_misc.release();
+  c->ident.release(); c->ident_n = 0;
   c->spts.release(); c->perm.release(); c->iperm.release(); c->nodes.release(); c->range.release();
   c->node_parent.release(); c->leaf_parent.release(); c->node_delta.release(); c->up.release(); c->arrivals.release(); c->root_box.release();
   c->label.release(); c->bprefix.release(); c->big_tops.release(); c->top.release();
@@ -1221,6 +1236,22 @@ int emst_context_set_exchange(emst_context* c, emst_exchange_fn fn, void* user) 
   if (!c) return EMST_ERR_PARAM;
   c->exch_fn = fn;
   c->exch_user = user;
+  return EMST_OK;
+}
+
+int emst_tree_token(emst_context* c, int64_t* token) {
+  if (!c || !token) return EMST_ERR_PARAM;
+  *token = c->tree_valid ? c->tree_token : 0;
+  return EMST_OK;
+}
+int emst_context_reuse_tree(emst_context* c, int64_t token) {
+  if (!c) return EMST_ERR_PARAM;
+  c->reuse_token = token;
+  return EMST_OK;
+}
+int emst_context_set_state_on_device(emst_context* c, int on) {
+  if (!c) return EMST_ERR_PARAM;
+  c->state_on_device = on != 0;
   return EMST_OK;
 }
 
@@ -1565,6 +1596,30 @@ int emst_build(emst_context* c, const float* pts, int64_t n, int32_t d, int32_t 
 
 namespace {
 
+// coarsening check of the kept proofs: a previous label l names a point of its component (the
+// reference's labels are member indices); every slot must share its new label with the slot of
+// that point, iperm[l] (any violation, of either kind, -> *flag: the proofs are dropped)
+__global__ void k_bb_check(const int* __restrict__ prev, const int* __restrict__ label,
+                           const unsigned* __restrict__ iperm, long long n, int* __restrict__ flag) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  const int l = prev[s];
+  const unsigned r = iperm[l];
+  if (prev[r] != l || label[r] != label[s]) *flag = 1;
+}
+// every point its own component (labels are the points' own indices): *flag = 1 otherwise
+__global__ void k_bb_singletons(const int* __restrict__ label, const unsigned* __restrict__ perm, long long n,
+                                int* __restrict__ flag) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s < n && label[s] != (int)perm[s]) *flag = 1;
+}
+
+template <class Node>
+__global__ void k_reset_node_labels(Node* __restrict__ nodes, long long m) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < m) *reinterpret_cast<int2*>(&nodes[i].ref.z) = make_int2(kMixed, kMixed);
+}
+
 __global__ void k_labels_to_slots(const long long* __restrict__ labels_pt, const unsigned* __restrict__ perm, long long n,
                                   int* __restrict__ label_slot) {
   long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -1591,13 +1646,53 @@ __global__ void k_export_node_labels(const Node* __restrict__ nodes, long long m
 
 void prepare_labels_from_host(emst_context* c, const int64_t* labels, long long n) {
   ensure_rounds(c, n);
+  CK(cudaMemsetAsync(c->nfn_lb.p, 0, n * sizeof(float), c->stream));
+  if (c->state_on_device) {   // caller's device array: no staging
+    launch(c, k_labels_to_slots, grid_for(n, 256), 256, 0, (const long long*)labels, (const unsigned*)c->perm.p, n,
+           c->label.p);
+    return;
+  }
   DevBuf<long long> lab;
   lab.ensure(n);
   CK(cudaMemcpyAsync(lab.p, labels, n * sizeof(long long), cudaMemcpyHostToDevice, c->stream));
   launch(c, k_labels_to_slots, grid_for(n, 256), 256, 0, (const long long*)lab.p, (const unsigned*)c->perm.p, n, c->label.p);
-  CK(cudaMemsetAsync(c->nfn_lb.p, 0, n * sizeof(float), c->stream));
   CK(cudaStreamSynchronize(c->stream));
   lab.release();
+}
+
+// The tree a building block works on: the context's current one when the
+// caller named it (emst_context_reuse_tree, one call), else built from pts.
+void tree_for_call(emst_context* c, const float* pts, long long n, int d) {
+  const bool reuse = c->reuse_token != 0 && c->reuse_token == c->tree_token && c->tree_valid && c->n == n &&
+                     c->dim == d;
+  c->reuse_token = 0;
+  if (reuse) return;
+  const float* dp = stage_points(c, pts, n, d, 0, nullptr);
+  build_tree(c, dp, n, d);
+}
+
+// f64 bound bits of the device state -> the traversal's u64 radii (inf / NaN / negative: none)
+__global__ void k_bounds_in(const double* __restrict__ ub, long long n, bool use, unsigned long long* __restrict__ bits) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double w = use ? ub[i] : __longlong_as_double(0x7ff0000000000000ll);
+  bits[i] = (w >= 0.0 && w < __longlong_as_double(0x7ff0000000000000ll)) ? (unsigned long long)__double_as_longlong(w) : ~0ull;
+}
+__global__ void k_bounds_out(const unsigned long long* __restrict__ bits, long long n, double* __restrict__ ub) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long b = bits[i] >= 0x7ff0000000000000ull ? 0x7ff0000000000000ull : bits[i];
+  ub[i] = __longlong_as_double((long long)b);
+}
+__global__ void k_best_out(const EdgeKey* __restrict__ best, long long n, long long* __restrict__ bu,
+                           long long* __restrict__ bv, double* __restrict__ bw) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const EdgeKey k = best[i];
+  const bool none = k.uv == ~0ull;
+  bu[i] = none ? -1 : (long long)(k.uv >> 32);
+  bv[i] = none ? -1 : (long long)(k.uv & 0xffffffffull);
+  bw[i] = none ? __longlong_as_double(0x7ff0000000000000ll) : __longlong_as_double((long long)k.w);
 }
 
 }  // namespace
@@ -1609,22 +1704,26 @@ int emst_reduce_labels(emst_context* c, const float* pts, int64_t n, int32_t d, 
   try {
     set_device(c);
     check_shape(n, d);
-    const float* dp = stage_points(c, pts, n, d, 0, nullptr);
-    build_tree(c, dp, n, d);
+    tree_for_call(c, pts, n, d);
     if (n == 1) return EMST_OK;
     prepare_labels_from_host(c, labels, n);
     round_prepare(c, n, false, nullptr, nullptr);
     DevBuf<long long> il;
-    il.ensure(n - 1);
+    long long* ild = reinterpret_cast<long long*>(internal_labels);
+    if (!c->state_on_device) {
+      il.ensure(n - 1);
+      ild = il.p;
+    }
     if (d == 3)
       launch(c, k_export_node_labels<Node3>, grid_for(n - 1, 256), 256, 0, (const Node3*)reinterpret_cast<Node3*>(c->nodes.p),
              n - 1, (const long long*)nullptr, (const unsigned*)c->perm.p, (const int*)c->node_parent.p,
-             (const int*)c->label.p, (const int2*)c->range.p, (const int*)c->bprefix.p, il.p);
+             (const int*)c->label.p, (const int2*)c->range.p, (const int*)c->bprefix.p, ild);
     else
       launch(c, k_export_node_labels<Node2>, grid_for(n - 1, 256), 256, 0, (const Node2*)reinterpret_cast<Node2*>(c->nodes.p),
              n - 1, (const long long*)nullptr, (const unsigned*)c->perm.p, (const int*)c->node_parent.p,
-             (const int*)c->label.p, (const int2*)c->range.p, (const int*)c->bprefix.p, il.p);
-    CK(cudaMemcpyAsync(internal_labels, il.p, (n - 1) * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+             (const int*)c->label.p, (const int2*)c->range.p, (const int*)c->bprefix.p, ild);
+    if (!c->state_on_device)
+      CK(cudaMemcpyAsync(internal_labels, il.p, (n - 1) * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     il.release();
     return EMST_OK;
@@ -1639,13 +1738,17 @@ int emst_compute_upper_bounds(emst_context* c, const float* pts, int64_t n, int3
   try {
     set_device(c);
     check_shape(n, d);
-    const float* dp = stage_points(c, pts, n, d, 0, nullptr);
-    build_tree(c, dp, n, d);
+    tree_for_call(c, pts, n, d);
     prepare_labels_from_host(c, labels, n);
     CK(cudaMemsetAsync(c->ub.p, 0xff, n * sizeof(unsigned long long), c->stream));
     prepare_cores(c, n, 1, core);
     round_prepare(c, n, true, nullptr, nullptr);
     c->core = nullptr;
+    if (c->state_on_device) {
+      launch(c, k_bounds_out, grid_for(n, 256), 256, 0, (const unsigned long long*)c->ub.p, n, ub_out);
+      CK(cudaStreamSynchronize(c->stream));
+      return EMST_OK;
+    }
     std::vector<unsigned long long> bits(n);
     CK(cudaMemcpyAsync(bits.data(), c->ub.p, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1668,28 +1771,93 @@ int emst_find_component_outgoing_edges(emst_context* c, const float* pts, int64_
     set_device(c);
     check_shape(n, d);
     if (n < 2) fail(EMST_ERR_NOTHING, "a single component has no outgoing edges");
-    const float* dp = stage_points(c, pts, n, d, 0, nullptr);
-    build_tree(c, dp, n, d);
+    tree_for_call(c, pts, n, d);
     prepare_labels_from_host(c, labels, n);
-    std::vector<unsigned long long> bits(n);
-    for (long long i = 0; i < n; ++i) {
-      double w = (flags & EMST_UPPER_BOUNDS) ? ub[i] : __builtin_inf();
-      memcpy(&bits[i], &w, 8);
-      if (!(w >= 0.0) || w == __builtin_inf()) bits[i] = ~0ull;
+    if (c->state_on_device) {
+      launch(c, k_bounds_in, grid_for(n, 256), 256, 0, ub, n, (flags & EMST_UPPER_BOUNDS) != 0, c->ub.p);
+    } else {
+      std::vector<unsigned long long> bits(n);
+      for (long long i = 0; i < n; ++i) {
+        double w = (flags & EMST_UPPER_BOUNDS) ? ub[i] : __builtin_inf();
+        memcpy(&bits[i], &w, 8);
+        if (!(w >= 0.0) || w == __builtin_inf()) bits[i] = ~0ull;
+      }
+      CK(cudaMemcpyAsync(c->ub.p, bits.data(), n * sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
+      CK(cudaStreamSynchronize(c->stream));   // (bits is a local)
     }
-    CK(cudaMemcpyAsync(c->ub.p, bits.data(), n * sizeof(unsigned long long), cudaMemcpyHostToDevice, c->stream));
-    // node labels only (bounds are caller-provided)
-    round_prepare(c, n, false, nullptr, nullptr);
+    // node labels only (bounds are caller-provided).  With subtree_skip the labelling is
+    // the solve's frontier form over every node (pure subtrees become "inside", top pure
+    // nodes are recorded, so queries whose search box stays inside theirs settle at once);
+    // it starts from MIXED records, as after a build
+    const bool skip = flags & EMST_SUBTREE_SKIP;
+    if (skip && n > 1) {
+      if (d == 3) launch(c, k_reset_node_labels<Node3>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node3*>(c->nodes.p), n - 1);
+      else launch(c, k_reset_node_labels<Node2>, grid_for(n - 1, 256), 256, 0, reinterpret_cast<Node2*>(c->nodes.p), n - 1);
+      CK(cudaMemsetAsync(c->top.p, 0, n * sizeof(int), c->stream));
+      c->front_n = -1;
+    }
+    round_prepare(c, n, false, nullptr, nullptr, skip, skip ? kLabelsFrontier : kLabelsFull);
     CK(cudaMemsetAsync(c->best.p, 0xff, n * sizeof(EdgeKey), c->stream));
     CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
     prepare_cores(c, n, 1, core);
     c->one_side = false;
+    // nearest-foreign proofs (Euclidean, single rank): kept from the previous call on this tree
+    // when its components are coarsened by these, else started afresh
+    const bool proofs = (flags & EMST_UPPER_BOUNDS) && !core && c->world == 1 && c->vshards == 1 && c->proof_from > 0;
+    if (proofs) {
+      c->bb_nfn.ensure(n);
+      c->bb_prev.ensure(n);
+      bool keep = c->bb_token == c->tree_token;
+      if (keep) {
+        int* flag = reinterpret_cast<int*>(dev_counter(c, 15));
+        launch(c, k_bb_check, grid_for(n, 256), 256, 0, (const int*)c->bb_prev.p, (const int*)c->label.p,
+               (const unsigned*)c->iperm.p, (long long)n, flag);
+        read_counters(c);
+        keep = c->host_counters[15] == 0;
+        CK(cudaMemsetAsync(flag, 0, sizeof(long long), c->stream));
+      }
+      if (!keep) {
+        CK(cudaMemsetAsync(c->bb_nfn.p, 0, n * sizeof(float), c->stream));
+        c->bb_skip = 0.0;
+        c->bb_calls = 0;
+        // a chain starts: all singletons is the solve's round 1 (its own kernel)
+        int* flag = reinterpret_cast<int*>(dev_counter(c, 15));
+        launch(c, k_bb_singletons, grid_for(n, 256), 256, 0, (const int*)c->label.p, (const unsigned*)c->perm.p,
+               (long long)n, flag);
+        read_counters(c);
+        c->singleton_round = c->host_counters[15] == 0;
+        CK(cudaMemsetAsync(flag, 0, sizeof(long long), c->stream));
+      }
+      std::swap(c->nfn_lb, c->bb_nfn);
+      // the chain's k-th call runs as the solve's round k: the proof kernel from proof_from on,
+      // query lists once the previous call settled enough queries up front
+      c->round = c->bb_calls + 1;
+      c->skip_frac = c->bb_skip;
+    }
     round_find(c, n, n, flags);
+    c->singleton_round = false;
+    if (proofs) {
+      std::swap(c->nfn_lb, c->bb_nfn);
+      c->round = 0;
+      c->bb_calls++;
+      CK(cudaMemcpyAsync(c->bb_prev.p, c->label.p, n * sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+      c->bb_token = c->tree_token;
+    }
     c->core = nullptr;
+    if (c->state_on_device) {
+      launch(c, k_best_out, grid_for(n, 256), 256, 0, (const EdgeKey*)c->best.p, n, reinterpret_cast<long long*>(best_u),
+             reinterpret_cast<long long*>(best_v), best_w);
+      read_counters(c);
+      if (c->host_counters[3]) fail(EMST_ERR_STACK, "edge traversal exceeded %d stacked nodes", kStackCapacity);
+      if (leaf_evals) *leaf_evals = c->host_counters[0];
+      if (proofs) c->bb_skip = (double)c->host_counters[9] / (double)n;
+      return EMST_OK;
+    }
     std::vector<EdgeKey> keys(n);
     CK(cudaMemcpyAsync(keys.data(), c->best.p, n * sizeof(EdgeKey), cudaMemcpyDeviceToHost, c->stream));
     read_counters(c);
     if (c->host_counters[3]) fail(EMST_ERR_STACK, "edge traversal exceeded %d stacked nodes", kStackCapacity);
+    if (proofs) c->bb_skip = (double)c->host_counters[9] / (double)n;
     for (long long i = 0; i < n; ++i) {
       if (keys[i].uv == ~0ull) {
         best_u[i] = -1;
@@ -1704,6 +1872,11 @@ int emst_find_component_outgoing_edges(emst_context* c, const float* pts, int64_
     if (leaf_evals) *leaf_evals = c->host_counters[0];
     return EMST_OK;
   } catch (const Failure& f) {
+    if (c) {
+      c->bb_token = 0;   // (the proof buffers may be swapped)
+      c->round = 0;
+      c->singleton_round = false;
+    }
     if (c) cudaStreamSynchronize(c->stream);
     return finish(f, err, errlen);
   }
@@ -1717,6 +1890,127 @@ __global__ void k_cluster_min(const int* __restrict__ ptr, const long long* __re
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k < s) atomicMin(&cmin[ptr[k]], reps[k]);
 }
+
+// ---- merge_components on device state (all arrays device-resident)
+// dense[reps[k]] = k; err bit 1: a representative out of range, bit 2: listed twice
+__global__ void k_dense_map(const long long* __restrict__ reps, long long s, long long n, int* __restrict__ dense,
+                            int* __restrict__ err) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= s) return;
+  const long long r = reps[k];
+  if (r < 0 || r >= n) { atomicOr(err, 1); return; }
+  if (atomicExch(&dense[r], (int)k) != -1) atomicOr(err, 2);
+}
+// label[i] = dense[labels[i]]; err bit 4: a label that is not a listed representative
+__global__ void k_dense_labels(const long long* __restrict__ labels, long long n, const int* __restrict__ dense,
+                               int* __restrict__ label, int* __restrict__ err) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long l = labels[i];
+  const int k = (l >= 0 && l < n) ? dense[l] : -1;
+  if (k < 0) atomicOr(err, 4);
+  label[i] = k < 0 ? 0 : k;
+}
+// per dense component: its best edge as a 128-bit key; err bit 8: an endpoint out of range
+__global__ void k_keys_from_best(const long long* __restrict__ reps, long long s, const long long* __restrict__ bu,
+                                 const long long* __restrict__ bv, const double* __restrict__ bw, long long n,
+                                 EdgeKey* __restrict__ best, int* __restrict__ err) {
+  const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (k >= s) return;
+  const long long r = reps[k];
+  EdgeKey e;
+  e.uv = ~0ull;
+  e.w = ~0ull;
+  if (r >= 0 && r < n && bv[r] >= 0) {
+    const long long u = bu[r], v = bv[r];
+    if (u < 0 || u >= n || v >= n) atomicOr(err, 8);
+    else {
+      e.uv = ((unsigned long long)u << 32) | (unsigned long long)v;
+      e.w = (unsigned long long)__double_as_longlong(bw[r]);
+    }
+  }
+  best[k] = e;
+}
+// reference labels: every point adopts its cluster's smallest representative
+// (the dense slot labels were already relabelled by the merge: go through the input labels again)
+__global__ void k_labels_from_clusters(long long* __restrict__ labels, long long n, const int* __restrict__ dense,
+                                       const int* __restrict__ root, const long long* __restrict__ cmin) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) labels[i] = cmin[root[dense[labels[i]]]];
+}
+__global__ void k_edges_out(const EdgeKey* __restrict__ eout, long long ne, long long* __restrict__ ou,
+                            long long* __restrict__ ov, double* __restrict__ ow) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= ne) return;
+  const EdgeKey k = eout[e];
+  ou[e] = (long long)(k.uv >> 32);
+  ov[e] = (long long)(k.uv & 0xffffffffull);
+  ow[e] = __longlong_as_double((long long)k.w);
+}
+// new_reps: the representatives that are their cluster's minimum, in k (= ascending) order
+struct NewRepsOp {
+  using T = unsigned;
+  const int* root;
+  const long long* reps;
+  const long long* cmin;
+  long long* new_reps;
+  long long s;
+  __device__ void load(long long i0, int cnt, unsigned* v) const {
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j)
+      v[j] = j < cnt && cmin[root[i0 + j]] == reps[i0 + j] ? 1u : 0u;
+  }
+  __device__ void side(long long, int, const unsigned*) const {}
+  __device__ void store(long long i0, int cnt, const unsigned* v, unsigned ex) const {
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      if (j < cnt && v[j]) new_reps[ex] = reps[i0 + j];
+      ex += v[j];
+    }
+  }
+};
+
+// identity permutation of n (point order is the merge building block's "slot" order; the
+// tree's own iperm stays intact for the calls that reuse the tree)
+const unsigned* identity_perm(emst_context* c, long long n) {
+  if (c->ident_n < n) {
+    c->ident.ensure(n);
+    launch(c, k_iota_u32, grid_for(n, 256), 256, 0, c->ident.p, n);
+    c->ident_n = n;
+  }
+  return c->ident.p;
+}
+
+void merge_on_device(emst_context* c, long long n, const long long* reps, long long s, const long long* bu,
+                     const long long* bv, const double* bw, long long* labels, long long* out_u, long long* out_v,
+                     double* out_w, long long* n_edges, long long* new_reps, long long* n_new) {
+  int* dense = c->bprefix.p;   // (n ints; the merge does not use the boundary prefix)
+  int* err = reinterpret_cast<int*>(dev_counter(c, 2)) + 1;   // high word of counters[2]
+  CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
+  CK(cudaMemsetAsync(dense, 0xff, n * sizeof(int), c->stream));
+  launch(c, k_dense_map, grid_for(s, 256), 256, 0, reps, s, n, dense, err);
+  launch(c, k_dense_labels, grid_for(n, 256), 256, 0, (const long long*)labels, n, (const int*)dense, c->label.p, err);
+  launch(c, k_keys_from_best, grid_for(s, 256), 256, 0, reps, s, bu, bv, bw, n, c->best.p, err);
+  read_counters(c);
+  const int e = (int)((unsigned long long)c->host_counters[2] >> 32);
+  if (e & 1) fail(EMST_ERR_PARAM, "a representative is out of range [0, %lld)", n);
+  if (e & 2) fail(EMST_ERR_PARAM, "a representative is listed twice");
+  if (e & 4) fail(EMST_ERR_PARAM, "a label is not a listed representative");
+  if (e & 8) fail(EMST_ERR_PARAM, "a component's edge has an endpoint out of range");
+  long long emitted = 0;
+  const long long next = round_merge(c, n, s, 0, &emitted, nullptr, false, identity_perm(c, n));
+  if (next >= s) fail(EMST_ERR_NO_REDUCE, "merge did not reduce the component count");
+  long long* cmin = reinterpret_cast<long long*>(c->ub.p);   // (s words; the merge does not use the bounds)
+  CK(cudaMemsetAsync(cmin, 0x7f, s * sizeof(long long), c->stream));
+  launch(c, k_cluster_min, grid_for(s, 256), 256, 0, (const int*)c->root.p, reps, s, cmin);
+  launch(c, k_labels_from_clusters, grid_for(n, 256), 256, 0, labels, n, (const int*)dense, (const int*)c->root.p,
+         (const long long*)cmin);
+  run_scan(c, s, NewRepsOp{c->root.p, reps, cmin, new_reps, s}, false);
+  if (emitted) launch(c, k_edges_out, grid_for(emitted, 256), 256, 0, (const EdgeKey*)c->eout.p, emitted, out_u, out_v, out_w);
+  CK(cudaStreamSynchronize(c->stream));
+  *n_edges = emitted;
+  *n_new = next;
+}
 }  // namespace
 
 extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* reps, int64_t s, const int64_t* best_u,
@@ -1728,9 +2022,18 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
     set_device(c);
     if (s < 1 || n < 1) fail(EMST_ERR_PARAM, "empty merge");
     ensure_rounds(c, n);
-    c->iperm.ensure(n);
     c->counters.ensure(kCounters);
     if (s > n) fail(EMST_ERR_PARAM, "%lld representatives for %lld points", (long long)s, (long long)n);
+    if (c->state_on_device) {
+      long long ne = 0, nn = 0;
+      merge_on_device(c, n, reinterpret_cast<const long long*>(reps), s, reinterpret_cast<const long long*>(best_u),
+                      reinterpret_cast<const long long*>(best_v), best_w, reinterpret_cast<long long*>(labels),
+                      reinterpret_cast<long long*>(out_u), reinterpret_cast<long long*>(out_v), out_w, &ne,
+                      reinterpret_cast<long long*>(new_reps), &nn);
+      *n_edges = ne;
+      *n_new = nn;
+      return EMST_OK;
+    }
     std::vector<int> dense(n, -1), lab(n);
     for (long long k = 0; k < s; ++k) {
       const long long r = reps[k];
@@ -1754,14 +2057,11 @@ extern "C" int emst_merge_components(emst_context* c, int64_t n, const int64_t* 
       keys[k].uv = ((unsigned long long)best_u[r] << 32) | (unsigned long long)best_v[r];
       memcpy(&keys[k].w, &best_w[r], 8);
     }
-    std::vector<unsigned> ident(n);
-    for (long long i = 0; i < n; ++i) ident[i] = (unsigned)i;   // point order == "slot" order here
     CK(cudaMemcpyAsync(c->label.p, lab.data(), n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->iperm.p, ident.data(), n * sizeof(unsigned), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->best.p, keys.data(), s * sizeof(EdgeKey), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(c->counters.p, 0, kCounters * sizeof(long long), c->stream));
     long long emitted = 0;
-    long long next = round_merge(c, n, s, 0, &emitted);
+    long long next = round_merge(c, n, s, 0, &emitted, nullptr, false, identity_perm(c, n));
     if (next >= s) fail(EMST_ERR_NO_REDUCE, "merge did not reduce the component count");
     // reference labels: each cluster adopts its smallest representative
     DevBuf<long long> dreps, cmin;

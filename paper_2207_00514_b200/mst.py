@@ -70,13 +70,23 @@ class ComponentState:
     upper_bounds: np.ndarray
 
     @classmethod
-    def initial(cls, bvh: Bvh) -> "ComponentState":
+    def initial(cls, bvh: Bvh, device=None) -> "ComponentState":
+        """Every point its own component.  ``device`` (e.g. "cuda") keeps the state in HBM as torch
+        tensors: the building blocks then run round after round without host copies."""
         n = bvh.num_points
+        if device is not None:
+            import torch
+            dev = torch.device(device)
+            return cls(torch.arange(n, dtype=torch.int64, device=dev),
+                       torch.full((max(n - 1, 0),), MIXED, dtype=torch.int64, device=dev),
+                       torch.full((n,), math.inf, dtype=torch.float64, device=dev))
         return cls(np.arange(n, dtype=np.int64), np.full(max(n - 1, 0), MIXED, dtype=np.int64),
                    np.full(n, np.inf, dtype=np.float64))
 
     @property
     def num_components(self) -> int:
+        if _on_device(self.labels):
+            return int(_device_reps(self.labels).numel())
         return int(np.unique(self.labels).shape[0])
 
 
@@ -253,75 +263,184 @@ def boruvka_emst(points, metric="euclidean", k_pts: int = 1, *, threads: int = 0
 
 
 # ----------------------------------------------------- per-round building blocks
+# Each call runs on the native context that holds the Bvh's tree when there is
+# one (no rebuild while its token is current), and on device-resident state when
+# the state's arrays are CUDA tensors (ComponentState.initial(bvh, device="cuda")):
+# then nothing crosses PCIe but a few counters.
 
-def reduce_labels(bvh: Bvh, state: ComponentState) -> np.ndarray:
+def _on_device(x) -> bool:
+    try:
+        import torch
+    except ImportError:
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _device_reps(labels):
+    """np.unique of device labels (values in [0, n)) without a sort.  The reference's labels name a
+    member of their component that labels itself (its smallest index), so the representatives are
+    the fixed points i == labels[i] -- checked by one gather (labels[labels] == labels); anything
+    else goes through torch.unique."""
+    import torch
+    n = labels.shape[0]
+    if n == 0:
+        return labels.new_empty(0)
+    lo, hi = torch.aminmax(labels)
+    if int(lo) < 0 or int(hi) >= n:
+        raise InvalidParameterError(f"labels must lie in [0, {n})")
+    if bool(torch.equal(labels[labels], labels)):
+        return torch.nonzero(labels == torch.arange(n, device=labels.device)).view(-1)
+    return torch.unique(labels)
+
+
+def _dev_array(x, dtype_name: str, n: int, what: str):
+    """A contiguous CUDA tensor of `dtype_name` and length n (the device-state contract)."""
+    import torch
+    dt = getattr(torch, dtype_name)
+    if not _on_device(x) or x.dtype != dt or x.dim() != 1 or x.shape[0] != n:
+        raise DimensionMismatchError(f"{what} must be a CUDA {dtype_name} vector of length {n}")
+    return x if x.is_contiguous() else x.contiguous()
+
+
+class _Call:
+    """Context, tree reuse and state location for one building-block call."""
+
+    def __init__(self, bvh: Bvh | None, points, state):
+        self.device_state = _on_device(state.labels)
+        if self.device_state:
+            dev = state.labels.device.index
+            ctx = bvh.tree_context if bvh is not None and getattr(bvh.tree_context, "device", None) == dev else None
+            self.ctx = ctx if ctx is not None else _lib.default_context(dev)
+            self.ctx.after_torch(state.labels)
+        else:
+            ctx = bvh.tree_context if bvh is not None else None
+            self.ctx = ctx if ctx is not None else _lib.default_context()
+        # (token, points given to build(), the float32 array the tree was built from), set by build()
+        held = getattr(self.ctx, "tree_points", None)
+        self.token = 0
+        if bvh is not None and bvh.tree_context is self.ctx:
+            if points is None or points is bvh.points or (held is not None and held[0] == bvh.tree_token
+                                                          and held[1] is points):
+                self.token = bvh.tree_token
+        elif bvh is None and points is not None and held is not None and (held[1] is points or held[2] is points):
+            self.token = held[0]
+
+    def points(self, points):
+        """(keep-alive, pointer, n, d) of the points the call hands over.  With the tree reused they were
+        validated when it was built and are not read again: only their shape is checked."""
+        if self.token:
+            shape = tuple(points.shape) if hasattr(points, "shape") else np.asarray(points).shape
+            if len(shape) != 2:
+                raise DimensionMismatchError("points must be a 2-D array")
+            return None, None, int(shape[0]), int(shape[1])
+        pts = as_point_array(points)
+        return pts, pts.ctypes.data, pts.shape[0], pts.shape[1]
+
+    def __enter__(self):
+        self.ctx.lock.acquire()
+        if self.token:
+            self.ctx.reuse_tree(self.token)
+        self.ctx.state_on_device(self.device_state)
+        return self
+
+    def __exit__(self, *exc):
+        self.ctx.state_on_device(False)
+        self.ctx.reuse_tree(0)
+        self.ctx.lock.release()
+
+
+def reduce_labels(bvh: Bvh, state: ComponentState):
     """Internal-node labels, MIXED where children disagree (mst.py:436-448).
 
     The GPU derives node labels from slot-range boundary counts over the tree it
-    builds from ``bvh.points`` (recorded by :func:`.bvh.build`).
+    built for ``bvh`` (reused while it is the context's current tree, else rebuilt
+    from ``bvh.points``).
     """
     if state.labels.shape[0] != bvh.num_points:
         raise DimensionMismatchError("state does not match the hierarchy")
     if bvh.points is None:
         raise InvalidParameterError("reduce_labels needs a Bvh produced by build() (it carries its points)")
-    pts = as_point_array(bvh.points)
-    n = pts.shape[0]
+    n = bvh.num_points
     if n > 1:
-        lab = np.ascontiguousarray(state.labels, np.int64)
-        out = np.empty(n - 1, np.int64)
-        ctx = _lib.default_context()
+        call = _Call(bvh, None, state)
+        pts, pp, n, d = call.points(bvh.points)
         e = _lib.err_buf()
-        with ctx.lock:
-            rc = _lib.load().emst_reduce_labels(ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data,
-                                                out.ctypes.data, e, len(e))
+        if call.device_state:
+            lab = _dev_array(state.labels, "int64", n, "labels")
+            out = _dev_array(state.internal_labels, "int64", n - 1, "internal_labels")
+            lp, op = lab.data_ptr(), out.data_ptr()
+        else:
+            lab = np.ascontiguousarray(state.labels, np.int64)
+            out = np.empty(n - 1, np.int64)
+            lp, op = lab.ctypes.data, out.ctypes.data
+        with call:
+            rc = _lib.load().emst_reduce_labels(call.ctx.handle, pp, n, d, lp, op, e, len(e))
         _lib.raise_for(rc, e)
-        state.internal_labels[:] = out
+        if out is not state.internal_labels:
+            state.internal_labels[:] = out
     return state.internal_labels
 
 
-def compute_upper_bounds(state: ComponentState, z_order, points, metric=None) -> np.ndarray:
+def compute_upper_bounds(state: ComponentState, z_order, points, metric=None):
     """Seed radii from Z-adjacent cross-component pairs (mst.py:451-469)."""
-    pts = as_point_array(points)
-    n = pts.shape[0]
-    if state.labels.shape[0] != n or np.asarray(z_order).shape[0] != n:
+    call = _Call(None, points, state)
+    pts, pp, n, d = call.points(points)
+    if state.labels.shape[0] != n or len(z_order) != n:
         raise DimensionMismatchError("state, order, and points disagree on size")
-    lab = np.ascontiguousarray(state.labels, np.int64)
-    ub = np.empty(n, np.float64)
     core_keep, core_ptr = core_pointer(metric, n)
-    ctx = _lib.default_context()
     e = _lib.err_buf()
-    with ctx.lock:
-        rc = _lib.load().emst_compute_upper_bounds(ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data,
-                                                   core_ptr, ub.ctypes.data, e, len(e))
+    if call.device_state:
+        lab = _dev_array(state.labels, "int64", n, "labels")
+        ub = _dev_array(state.upper_bounds, "float64", n, "upper_bounds")
+        lp, up = lab.data_ptr(), ub.data_ptr()
+    else:
+        lab = np.ascontiguousarray(state.labels, np.int64)
+        ub = np.empty(n, np.float64)
+        lp, up = lab.ctypes.data, ub.ctypes.data
+    with call:
+        rc = _lib.load().emst_compute_upper_bounds(call.ctx.handle, pp, n, d, lp, core_ptr, up, e, len(e))
     _lib.raise_for(rc, e)
-    state.upper_bounds[:] = ub
+    if ub is not state.upper_bounds:
+        state.upper_bounds[:] = ub
     return state.upper_bounds
 
 
 def find_component_outgoing_edges(bvh: Bvh, points, state: ComponentState, metric=None, *,
                                   subtree_skip: bool = True, use_upper_bounds: bool = True) -> OutgoingEdges:
     """Cheapest edge leaving every live component (mst.py:472-514)."""
-    pts = as_point_array(points)
-    n = pts.shape[0]
-    if state.labels.shape[0] != n or pts.shape[1] != bvh.dim or bvh.num_points != n:
+    call = _Call(bvh, points, state)
+    pts, pp, n, d = call.points(points)
+    if state.labels.shape[0] != n or d != bvh.dim or bvh.num_points != n:
         raise DimensionMismatchError("state does not match the hierarchy")
-    reps = np.unique(state.labels).astype(np.int64)
-    if reps.shape[0] < 2:
-        raise NothingToFindError("a single component has no outgoing edges")
-    lab = np.ascontiguousarray(state.labels, np.int64)
-    ub = np.ascontiguousarray(state.upper_bounds, np.float64)
-    bu = np.empty(n, np.int64)
-    bv = np.empty(n, np.int64)
-    bw = np.empty(n, np.float64)
-    evals = ctypes.c_int64(0)
     flags = (_lib.SUBTREE_SKIP if subtree_skip else 0) | (_lib.UPPER_BOUNDS if use_upper_bounds else 0)
     core_keep, core_ptr = core_pointer(metric, n)
-    ctx = _lib.default_context()
+    evals = ctypes.c_int64(0)
     e = _lib.err_buf()
-    with ctx.lock:
+    if call.device_state:
+        import torch
+        lab = _dev_array(state.labels, "int64", n, "labels")
+        ub = _dev_array(state.upper_bounds, "float64", n, "upper_bounds")
+        reps = _device_reps(lab)
+        if reps.numel() < 2:
+            raise NothingToFindError("a single component has no outgoing edges")
+        bu = torch.empty(n, dtype=torch.int64, device=lab.device)
+        bv = torch.empty_like(bu)
+        bw = torch.empty(n, dtype=torch.float64, device=lab.device)
+        ptrs = (lab.data_ptr(), ub.data_ptr(), bu.data_ptr(), bv.data_ptr(), bw.data_ptr())
+    else:
+        reps = np.unique(state.labels).astype(np.int64)
+        if reps.shape[0] < 2:
+            raise NothingToFindError("a single component has no outgoing edges")
+        lab = np.ascontiguousarray(state.labels, np.int64)
+        ub = np.ascontiguousarray(state.upper_bounds, np.float64)
+        bu = np.empty(n, np.int64)
+        bv = np.empty(n, np.int64)
+        bw = np.empty(n, np.float64)
+        ptrs = (lab.ctypes.data, ub.ctypes.data, bu.ctypes.data, bv.ctypes.data, bw.ctypes.data)
+    with call:
         rc = _lib.load().emst_find_component_outgoing_edges(
-            ctx.handle, pts.ctypes.data, n, pts.shape[1], lab.ctypes.data, ub.ctypes.data, core_ptr, flags,
-            bu.ctypes.data, bv.ctypes.data, bw.ctypes.data, ctypes.byref(evals), e, len(e))
+            call.ctx.handle, pp, n, d, ptrs[0], ptrs[1], core_ptr, flags,
+            ptrs[2], ptrs[3], ptrs[4], ctypes.byref(evals), e, len(e))
     _lib.raise_for(rc, e)
     missing = reps[bv[reps] < 0]
     if missing.shape[0] > 0:
@@ -331,32 +450,51 @@ def find_component_outgoing_edges(bvh: Bvh, points, state: ComponentState, metri
 
 def merge_components(state: ComponentState, outgoing: OutgoingEdges) -> MergeOutcome:
     """Collapse the chosen-edge graph; relabel in place (mst.py:517-547)."""
-    reps = np.ascontiguousarray(outgoing.reps, np.int64)
     n = state.labels.shape[0]
-    s = reps.shape[0]
-    lab = np.ascontiguousarray(state.labels, np.int64).copy()
-    ou = np.empty(max(s, 1), np.int64)
-    ov = np.empty(max(s, 1), np.int64)
-    ow = np.empty(max(s, 1), np.float64)
-    nr = np.empty(max(s, 1), np.int64)
+    call = _Call(None, None, state)
     ne = ctypes.c_int64(0)
     nn = ctypes.c_int64(0)
-    bu = np.ascontiguousarray(outgoing.u, np.int64)
-    bv = np.ascontiguousarray(outgoing.v, np.int64)
-    bw = np.ascontiguousarray(outgoing.w, np.float64)
-    ctx = _lib.default_context()
     e = _lib.err_buf()
-    with ctx.lock:
-        rc = _lib.load().emst_merge_components(ctx.handle, n, reps.ctypes.data, s, bu.ctypes.data, bv.ctypes.data,
-                                               bw.ctypes.data, lab.ctypes.data, ou.ctypes.data, ov.ctypes.data,
-                                               ow.ctypes.data, ctypes.byref(ne), nr.ctypes.data, ctypes.byref(nn),
-                                               e, len(e))
+    if call.device_state:
+        import torch
+        s = int(outgoing.reps.shape[0])
+        reps = _dev_array(outgoing.reps, "int64", s, "reps")
+        lab = _dev_array(state.labels, "int64", n, "labels")
+        bu = _dev_array(outgoing.u, "int64", n, "u")
+        bv = _dev_array(outgoing.v, "int64", n, "v")
+        bw = _dev_array(outgoing.w, "float64", n, "w")
+        dev = lab.device
+        ou = torch.empty(max(s, 1), dtype=torch.int64, device=dev)
+        ov = torch.empty_like(ou)
+        ow = torch.empty(max(s, 1), dtype=torch.float64, device=dev)
+        nr = torch.empty_like(ou)
+        ptrs = [t.data_ptr() for t in (reps, bu, bv, bw, lab, ou, ov, ow, nr)]
+    else:
+        reps = np.ascontiguousarray(outgoing.reps, np.int64)
+        s = reps.shape[0]
+        lab = np.ascontiguousarray(state.labels, np.int64).copy()
+        ou = np.empty(max(s, 1), np.int64)
+        ov = np.empty(max(s, 1), np.int64)
+        ow = np.empty(max(s, 1), np.float64)
+        nr = np.empty(max(s, 1), np.int64)
+        bu = np.ascontiguousarray(outgoing.u, np.int64)
+        bv = np.ascontiguousarray(outgoing.v, np.int64)
+        bw = np.ascontiguousarray(outgoing.w, np.float64)
+        ptrs = [a.ctypes.data for a in (reps, bu, bv, bw, lab, ou, ov, ow, nr)]
+    with call:
+        rc = _lib.load().emst_merge_components(call.ctx.handle, n, ptrs[0], s, ptrs[1], ptrs[2], ptrs[3], ptrs[4],
+                                               ptrs[5], ptrs[6], ptrs[7], ctypes.byref(ne), ptrs[8],
+                                               ctypes.byref(nn), e, len(e))
     if rc == 5:
         raise InternalInvariantViolation("a component's chosen edge is inconsistent")
     _lib.raise_for(rc, e)
-    state.labels[:] = lab
+    if lab is not state.labels:
+        state.labels[:] = lab
     k, m = ne.value, nn.value
-    return MergeOutcome(int(m), ou[:k].copy(), ov[:k].copy(), ow[:k].copy(), nr[:m].copy())
+    return MergeOutcome(int(m), ou[:k].clone() if call.device_state else ou[:k].copy(),
+                        ov[:k].clone() if call.device_state else ov[:k].copy(),
+                        ow[:k].clone() if call.device_state else ow[:k].copy(),
+                        nr[:m].clone() if call.device_state else nr[:m].copy())
 
 
 def iteration_bound(n: int) -> int:
