@@ -56,7 +56,7 @@ def hbm_peak():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r01_traverse_traffic.json")
+TRAFFIC_PATH = os.path.join(ROOT, "profiles", "r02_traverse_traffic.json")
 
 
 def measured_traffic(cfg: str):
@@ -310,6 +310,12 @@ def run_ours(args):
     trav_bytes = (12 * d + 36) * st.traverse_queries
     trav_gbs = trav_bytes / (st.traverse_ms / 1e3) / 1e9 if st.traverse_ms > 0 else 0.0
     whole_bytes = algorithmic_bytes(n, d, counts)
+    # every rank's phase times (the replicated phases bound the multi-GPU speed-up)
+    phases = {k: round(st.phase_ms[i], 3) for i, k in enumerate(E._lib.PHASES)}
+    rank_phases = [phases]
+    if dist is not None:
+        rank_phases = [None] * world
+        dist.all_gather_object(rank_phases, phases)
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -339,7 +345,8 @@ def run_ours(args):
         "iterations": int(st.iterations), "component_counts": counts,
         "rounds": [{"traverse_ms": round(st.round_traverse_ms[i], 3), "node_visits": int(st.round_node_visits[i]),
                     "found": int(st.round_found[i]), "skipped": int(st.round_skipped[i])} for i in range(min(st.iterations, 64))],
-        "phase_ms": {k: round(st.phase_ms[i], 3) for i, k in enumerate(E._lib.PHASES)},
+        "phase_ms": phases,
+        "rank_phase_ms": rank_phases if world > 1 else None,
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:

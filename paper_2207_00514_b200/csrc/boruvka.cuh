@@ -143,6 +143,48 @@ struct RoundScanOp {
   }
 };
 
+// The boundary-pair seeds of RoundScanOp::side for the pairs (s, s + 1) whose left
+// slot s lies in [q0, q1): a rank of a multi-GPU solve seeds only its own Morton
+// range (the ranges tile [0, n - 1), so the min-allreduce of the bounds that
+// follows gives every rank the replicated result).  8 slots per thread.
+template <int D>
+__global__ void __launch_bounds__(kScanThreads) k_seed_boundary(const int* __restrict__ label,
+                                                                const float4* __restrict__ spts, long long n,
+                                                                long long q0, long long q1,
+                                                                const double* __restrict__ core,
+                                                                unsigned long long* ub) {
+  const long long i0 = q0 + (blockIdx.x * (long long)blockDim.x + threadIdx.x) * kScanItems;
+  const int cnt = i0 >= q1 ? 0 : (int)min((long long)kScanItems, q1 - i0);
+  int lab[kScanItems + 1];
+#pragma unroll
+  for (int j = 0; j <= kScanItems; ++j) lab[j] = j <= cnt && i0 + j < n ? label[i0 + j] : -1;
+  unsigned long long wb[kScanItems];
+  bool v[kScanItems];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    v[j] = j < cnt && i0 + j + 1 < n && lab[j] != lab[j + 1];
+    wb[j] = ~0ull;
+    if (v[j]) {
+      const float4 a = __ldg(spts + i0 + j), b = __ldg(spts + i0 + j + 1);
+      const float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
+      double w = exact_dist<D>(pa, pb);
+      if (core) w = fmax(w, fmax(core[i0 + j], core[i0 + j + 1]));   // mst.py:217-220
+      wb[j] = (unsigned long long)__double_as_longlong(w);
+    }
+  }
+  // one update per label among the thread's pairs: both ends of every boundary pair
+  int ul[2 * kScanItems];
+  unsigned long long uw[2 * kScanItems];
+#pragma unroll
+  for (int j = 0; j < kScanItems; ++j) {
+    ul[2 * j] = v[j] ? lab[j] : -1;
+    uw[2 * j] = wb[j];
+    ul[2 * j + 1] = v[j] ? lab[j + 1] : -1;
+    uw[2 * j + 1] = wb[j];
+  }
+  apply_bound_updates<2 * kScanItems>(ul, uw, ub);   // every lane of the warp takes part
+}
+
 // Round 1 of the solve: every slot is its own component (labels are the slot
 // ids), so the boundary-pair fold of the round scan reduces to
 // ub[s] = min(w(s-1, s), w(s, s+1)) with the same exact weights (mst.py:198-224):
@@ -213,12 +255,14 @@ __device__ __forceinline__ float seed_pairs(const float4* sp, const int* sl, uns
 template <int D, int kW>
 __global__ void __launch_bounds__(kSeedThreads) k_seed_window(const int* __restrict__ label,
                                                               const float4* __restrict__ spts, long long n, int W,
-                                                              unsigned long long* ub) {
+                                                              unsigned long long* ub, long long block0 = 0) {
+  // (block0: the first block of the launch -- a rank of a multi-GPU solve seeds the blocks
+  // that cover its Morton range; every slot's seed comes from the block holding the slot)
   __shared__ float4 sp[kSeedThreads + 2 * kSeedMaxW];
   __shared__ int sl[kSeedThreads + 2 * kSeedMaxW];
   __shared__ unsigned s_best[kSeedThreads];
   if (kW) W = kW;
-  const long long base = blockIdx.x * (long long)kSeedThreads;
+  const long long base = (block0 + blockIdx.x) * (long long)kSeedThreads;
   const int lim = kSeedThreads + 2 * W;
   for (int i = threadIdx.x; i < lim; i += kSeedThreads) {
     const long long g = base - W + i;

@@ -584,9 +584,15 @@ void launch_labels(emst_context* c, long long n, LabelMode mode, bool want_top) 
   c->front_pending = true;   // front_n is read back with the round's counters
 }
 
+void allreduce_u64(emst_context* c, unsigned long long* buf, long long count, int rows, long long stride, bool sum);
+
 void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds,
                    bool want_top = false, LabelMode mode = kLabelsFull) {
   c->top_valid = false;
+  // Ranks of a multi-GPU solve (rounds >= 2) seed the bounds of their own Morton range only and
+  // meet in one min-allreduce; round 1's streaming seeds and the building blocks stay replicated.
+  const bool sharded = bounds && c->world > 1 && c->round > 1;
+  const long long r0 = sharded ? c->rank * n / c->world : 0, r1 = sharded ? (c->rank + 1) * n / c->world : n;
   cudaEvent_t e0 = timer_event(c);
   if (mode == kLabelsNone && c->round == 1) {
     // round 1 of the solve: singletons, no node labels, so no boundary prefix either
@@ -595,7 +601,15 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
       else launch(c, k_seed_round1<2>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, c->core, c->ub.p);
     }
   } else {
-    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds, c->core}, false);
+    // ranks of a multi-GPU solve seed only their own Morton range (below), so the scan then
+    // just counts the boundaries
+    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds && !sharded, c->core},
+             false);
+  }
+  if (sharded && r1 > r0) {
+    const unsigned g = grid_for((r1 - r0 + kScanItems - 1) / kScanItems, kScanThreads);
+    if (c->dim == 3) launch(c, k_seed_boundary<3>, g, kScanThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, r0, r1, c->core, c->ub.p);
+    else launch(c, k_seed_boundary<2>, g, kScanThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, r0, r1, c->core, c->ub.p);
   }
   // window seeds pay while components are small and in 3D (measured: 37M blobs 3D
   // -2.3 ms, 10M normal 3D -0.6 ms; the 2D configs lose ~1 %); later rounds gain nothing
@@ -603,9 +617,12 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
     const int W = std::min(c->seed_window, kSeedMaxW);
     const auto kern = c->dim == 3 ? (W == 8 ? k_seed_window<3, 8> : k_seed_window<3, 0>)
                                   : (W == 8 ? k_seed_window<2, 8> : k_seed_window<2, 0>);
-    launch(c, kern, grid_for(n, kSeedThreads), kSeedThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, W,
-           c->ub.p);
+    const long long b0 = r0 / kSeedThreads, b1 = (r1 + kSeedThreads - 1) / kSeedThreads;   // blocks covering [r0, r1)
+    launch(c, kern, (unsigned)std::max<long long>(1, b1 - b0), kSeedThreads, 0, (const int*)c->label.p,
+           (const float4*)c->spts.p, n, W, c->ub.p, b0);
   }
+  // the ranks' seeds meet in one min-allreduce of the c bounds (u64 bit patterns)
+  if (sharded) allreduce_u64(c, c->ub.p, c->round_comps, 1, 0, false);
   cudaEvent_t e1 = timer_event(c);
   if (n > 1 && mode != kLabelsNone) {
     if (c->dim == 3) launch_labels<Node3>(c, n, mode, want_top);

@@ -70,8 +70,10 @@ def main(tag):
             out.append(f"## Step composition, {cfg} (`{tag}_launches_{cfg}.csv`)\n")
             out.append(capture("launch_summary.py", p))
             out.append("")
-    traffic_path = os.path.join(P, "r01_traverse_traffic.json")
-    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    traffic_path = os.path.join(P, f"{tag}_traverse_traffic.json")
+    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {
+        "note": "DRAM bytes of every k_traverse launch of one solve, from ncu --metrics dram__bytes_read.sum,"
+                "dram__bytes_write.sum (tools/evidence_r02.sh); bench.py reports dram_bytes_per_launch as roofline.traffic"}
     for cfg in ("blobs3d_37m", "blobs2d_24m"):
         p = os.path.join(G, f"trav_dram_{cfg}.csv")
         if os.path.exists(p):
