@@ -75,6 +75,17 @@ __device__ __forceinline__ void apply_bound_updates(int* ul, unsigned long long*
   }
 }
 
+// A boundary pair's contribution to a component bound.  The building block
+// compute_upper_bounds returns the reference's exact f64 weights (mst.py:198-224);
+// inside the solve a bound only has to be at least a real edge's weight (H3), so
+// an f32 upper bound (every operation rounded up, then 2^-40 of slack over the
+// f64 rounding of the exact weight) replaces the f64 distance and its sqrt.
+template <int D>
+__device__ __forceinline__ unsigned long long seed_weight(const float* pa, const float* pb, bool exact) {
+  if (exact) return (unsigned long long)__double_as_longlong(exact_dist<D>(pa, pb));
+  return (unsigned long long)__double_as_longlong(__dmul_ru((double)__fsqrt_ru(point_ub2<D>(pa, pb)), 1.0 + 0x1p-40));
+}
+
 struct RoundScanOp {
   using T = unsigned;
   const int* label;
@@ -85,6 +96,7 @@ struct RoundScanOp {
   int dim;
   bool bounds;
   const double* core;   // mutual reachability (slot order), or nullptr
+  bool exact;           // exact f64 weights (the building block) or upper bounds (the solve)
   __device__ void load(long long i0, int cnt, unsigned* v) const {
     int lab[kScanItems + 1];
 #pragma unroll
@@ -109,9 +121,10 @@ struct RoundScanOp {
       if (v[j]) {
         const float4 a = __ldg(spts + i0 + j), b = __ldg(spts + i0 + j + 1);
         const float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
-        double w = dim == 3 ? exact_dist<3>(pa, pb) : exact_dist<2>(pa, pb);
-        if (core) w = fmax(w, fmax(core[i0 + j], core[i0 + j + 1]));   // mst.py:217-220
-        wb[j] = (unsigned long long)__double_as_longlong(w);
+        wb[j] = dim == 3 ? seed_weight<3>(pa, pb, exact) : seed_weight<2>(pa, pb, exact);
+        if (core)   // mst.py:217-220
+          wb[j] = (unsigned long long)__double_as_longlong(
+              fmax(__longlong_as_double((long long)wb[j]), fmax(core[i0 + j], core[i0 + j + 1])));
       }
     }
     // One update per run of equal labels among the thread's 9 slots: the min of
@@ -167,7 +180,7 @@ __global__ void __launch_bounds__(kScanThreads) k_seed_boundary(const int* __res
     if (v[j]) {
       const float4 a = __ldg(spts + i0 + j), b = __ldg(spts + i0 + j + 1);
       const float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
-      double w = exact_dist<D>(pa, pb);
+      double w = __longlong_as_double((long long)seed_weight<D>(pa, pb, false));
       if (core) w = fmax(w, fmax(core[i0 + j], core[i0 + j + 1]));   // mst.py:217-220
       wb[j] = (unsigned long long)__double_as_longlong(w);
     }
@@ -187,7 +200,7 @@ __global__ void __launch_bounds__(kScanThreads) k_seed_boundary(const int* __res
 
 // Round 1 of the solve: every slot is its own component (labels are the slot
 // ids), so the boundary-pair fold of the round scan reduces to
-// ub[s] = min(w(s-1, s), w(s, s+1)) with the same exact weights (mst.py:198-224):
+// ub[s] = min(w(s-1, s), w(s, s+1)) (mst.py:198-224; f32 upper bounds of the weights, seed_weight):
 // one streaming pass, no atomics, and no boundary prefix (round 1 labels no nodes).
 template <int D>
 __global__ void k_seed_round1(const float4* __restrict__ spts, long long n, const double* __restrict__ core,
@@ -200,14 +213,14 @@ __global__ void k_seed_round1(const float4* __restrict__ spts, long long n, cons
   if (s > 0) {
     const float4 b = spts[s - 1];
     const float pb[3] = {b.x, b.y, b.z};
-    double d = exact_dist<D>(pb, pa);
+    double d = __longlong_as_double((long long)seed_weight<D>(pb, pa, false));   // (an upper bound suffices)
     if (core) d = fmax(d, fmax(core[s - 1], core[s]));
     w = d;
   }
   if (s + 1 < n) {
     const float4 b = spts[s + 1];
     const float pb[3] = {b.x, b.y, b.z};
-    double d = exact_dist<D>(pa, pb);
+    double d = __longlong_as_double((long long)seed_weight<D>(pa, pb, false));
     if (core) d = fmax(d, fmax(core[s], core[s + 1]));
     w = fmin(w, d);
   }

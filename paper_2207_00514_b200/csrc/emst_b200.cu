@@ -603,7 +603,9 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
   } else {
     // ranks of a multi-GPU solve seed only their own Morton range (below), so the scan then
     // just counts the boundaries
-    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds && !sharded, c->core},
+    // (exact weights for the building block compute_upper_bounds, round 0; upper bounds in the solve)
+    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds && !sharded, c->core,
+                               c->round == 0},
              false);
   }
   if (sharded && r1 > r0) {
