@@ -164,6 +164,9 @@ constexpr long long kTravPrefetch = EMST_TRAV_PREFETCH;   // L2 prefetch lookahe
 constexpr int kTraverseChunk = EMST_TRAV_CHUNK;   // consecutive Morton queries a warp claims at once
 constexpr int kSmemStack = EMST_SMEM_STACK;       // stack entries per lane kept in shared memory
 constexpr int kRefillIdle = EMST_REFILL_IDLE;   // refill when this many lanes are idle (or all are)
+#ifndef EMST_REFRESH_BY_VISITS
+#define EMST_REFRESH_BY_VISITS 1
+#endif
 #ifndef EMST_RADIUS_REFRESH
 #define EMST_RADIUS_REFRESH 256
 #endif
@@ -551,8 +554,13 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     }
     if (s < 0 || done) continue;
 
+#if EMST_REFRESH_BY_VISITS
+    // (the lane's visit counter doubles as the refresh clock: one increment per step less)
+    if (kBounds && !(kSingle || singletons) && (visits & (kRadiusRefresh - 1)) == kRadiusRefresh - 1) {
+#else
     if (kBounds && !(kSingle || singletons) && ++since_refresh >= kRadiusRefresh) {
       since_refresh = 0;
+#endif
       const double shared = bits_to_radius(__ldcg(&ub[comp]));
       if (shared < radius) { radius = shared; r2 = fminf(r2, prune_r2(shared)); }
     }
