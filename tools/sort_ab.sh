@@ -1,5 +1,15 @@
+# onesweep A/B (developer tool): summed k_onesweep ncu time for the default build and build_variants/*.so
+cd $GRAFT_REPO_ROOT
 for lib in default build_variants/*.so; do
   if [ "$lib" = default ]; then unset EMST_LIB_PATH; else export EMST_LIB_PATH=$PWD/$lib; fi
-  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_onesweep --csv --log-file gpurun_out/sort_$(basename $lib .so).csv python bench.py --profile --config blobs3d_37m > /dev/null 2>&1
+  ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_onesweep --csv \
+      --log-file gpurun_out/sab.csv python bench.py --profile --config ${CFG:-blobs3d_37m} > /dev/null 2>&1
+  python - "$lib" <<'PY'
+import csv, sys
+rows = list(csv.reader(open('gpurun_out/sab.csv'))); h = None; t = []
+for r in rows:
+    if 'Kernel Name' in r: h = r; continue
+    if h and len(r) == len(h): t.append(float(r[h.index('Metric Value')]) / 1e3)
+print(sys.argv[1], len(t), 'passes', round(sum(t) / 1e3, 3), 'ms', [round(x) for x in t])
+PY
 done
-REPS=1 bash tools/ab.sh
