@@ -54,5 +54,12 @@ while state.num_components > 1:
     out = E.find_component_outgoing_edges(bvh, pts, state)
     res = E.merge_components(state, out)
     edges += res.edges_u.shape[0] if hasattr(res, "edges_u") else 0
-print("ok mrd, ties, building blocks", flush=True)
+# the same loop on device-resident state (tree reuse, GPU merge, kept proofs)
+state = E.ComponentState.initial(bvh, device="cuda")
+while state.num_components > 1:
+    E.reduce_labels(bvh, state)
+    E.compute_upper_bounds(state, bvh.leaf_perm, pts)
+    out = E.find_component_outgoing_edges(bvh, pts, state)
+    res = E.merge_components(state, out)
+print("ok mrd, ties, building blocks (host and device state)", flush=True)
 print("SANITIZE DONE", flush=True)
