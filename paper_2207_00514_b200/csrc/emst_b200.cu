@@ -644,7 +644,20 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
   auto kernel = k_traverse<D, S, B, M, P, G>;
   int per_sm = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kTraverseThreads, 0));
-  const long long warps_needed = (q1 - q0 + kTraverseChunk - 1) / kTraverseChunk;
+  // Small launches (fewer queries than two per resident lane) claim half chunks, so that more
+  // warps start at once: there each query's chain of L2 round trips, not throughput, is the time
+  // (listed rounds: the list is about the share of queries the last round did not settle up front)
+  const bool listed = P && B && !M && c->round > 1 && c->skip_frac >= c->list_skip;
+  const double expect = listed ? std::max(0.0, 1.0 - c->skip_frac) * (double)(q1 - q0) : (double)(q1 - q0);
+  const long long resident_warps = (long long)c->num_sms * std::max(per_sm, 1) * (kTraverseThreads / 32);
+#ifdef EMST_CLAIM_FIXED
+  const int claim = kTraverseChunk;   // (A/B build)
+  (void)expect;
+  (void)resident_warps;
+#else
+  const int claim = expect <= (double)(resident_warps * kTraverseChunk) ? kTraverseChunk / 2 : kTraverseChunk;
+#endif
+  const long long warps_needed = (q1 - q0 + claim - 1) / claim;
   const long long blocks_needed = (warps_needed + kTraverseThreads / 32 - 1) / (kTraverseThreads / 32);
   const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((long long)c->num_sms * std::max(per_sm, 1),
                                                                              blocks_needed));
@@ -671,7 +684,7 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
            reinterpret_cast<int*>(dev_counter(c, 3)), work, c->singleton_round && c->vshards == 1 && c->world == 1,
            c->nfn_lb.p, (const int2*)c->up.p, (const int*)c->leaf_parent.p, (const Scene*)c->scene.p,
            c->top_valid ? (const int*)c->top.p : (const int*)nullptr, c->core, side,
-           use_list ? (const int*)c->qlist.p : (const int*)nullptr, (const unsigned*)qcount);
+           use_list ? (const int*)c->qlist.p : (const int*)nullptr, (const unsigned*)qcount, claim);
   }
   c->timers.push_back({ta, timer_event(c), nullptr, true, c->round, q0, q1});   // traverse_ms at the next sync
   c->traverse_launches++;

@@ -312,7 +312,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
            unsigned long long* __restrict__ work_counter, bool singletons, float* __restrict__ nfn_lb,
            const int2* __restrict__ up, const int* __restrict__ leaf_parent, const Scene* __restrict__ scene_ptr,
            const int* __restrict__ top_pure_in, const double* __restrict__ core_in, const int* __restrict__ side_in,
-           const int* __restrict__ qlist_in, const unsigned* __restrict__ qcount) {
+           const int* __restrict__ qlist_in, const unsigned* __restrict__ qcount, int claim) {
   // round 1 (kSingle) has no pure nodes, no one-sided round, no query list and no earlier proofs
   const int* __restrict__ top_pure = kSingle ? nullptr : top_pure_in;
   // (query lists and the one-sided last round come with the proof kernels only)
@@ -328,7 +328,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
   const Scene sc = *scene_ptr;
   const int skip_comp = side ? *side : -1;   // last round: the component whose queries are not run
 
-  // The warp claims kTraverseChunk consecutive Morton slots at a time and stages
+  // The warp claims `claim` (<= kTraverseChunk) consecutive Morton slots at a time and stages
   // their point, label, leaf parent, starting radius, proven nearest-foreign
   // bound and top pure node in shared memory with coalesced loads.
   constexpr int W = kTraverseThreads / 32;
@@ -438,7 +438,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       if (pool_next >= pool_end && !exhausted) {
         unsigned long long base = 0;
         if (lane == 0) {
-          base = atomicAdd(work_counter, (unsigned long long)kTraverseChunk);
+          base = atomicAdd(work_counter, (unsigned long long)claim);
 #if EMST_TRAV_PREFETCH
           // Warm L2 for the queries kTravPrefetch slots ahead: the low tree levels
           // they start in are the node records of about the same indices (Karras
@@ -471,7 +471,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
         } else {
           chunk_base = (int)base;
           pool_next = chunk_base;
-          pool_end = min(chunk_base + kTraverseChunk, total);
+          pool_end = min(chunk_base + claim, total);
           __syncwarp();
 #pragma unroll
           for (int j = 0; j < kTraverseChunk / 32; ++j) {
