@@ -129,7 +129,9 @@ constexpr int kTraverseThreads = EMST_TRAV_THREADS;
 // blocks could only pick 80 registers / 24 warps or 64 with 102 B of spills:
 // 37M blobs 3D -1.3 ms for 128 x 7).  Every other variant fits 64 registers
 // (8 blocks, 32 warps); 2D lanes prefer the extra warps (-17 % vs 48 warps less).
-// Round 1 (kSingle, 8 blocks) and the 3D round-2 kernel (no proof, 7) have their own knobs.
+// Round 1 (kSingle, 8 blocks) and the 3D round-2 kernel (no proof) have their own knobs; the
+// round-2 kernel runs 8 blocks at 64 registers (28 B of spills) since its radius refresh is
+// clocked by the visit counter: round 2 at 37M blobs 3D 11.58 -> 11.14 ms.
 #ifndef EMST_TRAV_MINB3
 #define EMST_TRAV_MINB3 7
 #endif
@@ -137,7 +139,7 @@ constexpr int kTraverseThreads = EMST_TRAV_THREADS;
 #define EMST_TRAV_MINB3S 8
 #endif
 #ifndef EMST_TRAV_MINB3R2
-#define EMST_TRAV_MINB3R2 7
+#define EMST_TRAV_MINB3R2 8
 #endif
 #ifndef EMST_TRAV_MINB2S
 #define EMST_TRAV_MINB2S 9
