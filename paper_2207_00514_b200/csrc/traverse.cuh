@@ -175,12 +175,13 @@ template <int D> constexpr int kRefillIdle = D == 3 ? EMST_REFILL_IDLE3 : EMST_R
 #define EMST_REFRESH_BY_VISITS 1
 #endif
 #ifndef EMST_RADIUS_REFRESH
-#define EMST_RADIUS_REFRESH 256
+#define EMST_RADIUS_REFRESH 4096
 #endif
-// pops between re-reads of the component's shared radius (the first one after
-// half of it).  Measured at 37M blobs 3D: every 16 pops 72.4 ms, 32: 71.8, 64:
-// 71.4, 256 (in practice only very long searches re-read): 70.6 -- an L2 read
-// per lane costs more than the slightly tighter radius saves.
+// visits between re-reads of the component's shared radius (the lane's visit
+// counter is the clock).  Measured at 37M blobs 3D: every 16 pops 72.4 ms, 32:
+// 71.8, 64: 71.4, 256: 70.6 (round 1); round 2, traversal 43.8 ms at 256, 43.6 at
+// 512, 43.5 at 1024, 43.4 at 4096 and 43.3 at 65536 -- an L2 read per lane costs
+// more than the slightly tighter radius saves; only very long searches re-read.
 constexpr int kRadiusRefresh = EMST_RADIUS_REFRESH;
 #ifndef EMST_SHARE_AT_END
 #define EMST_SHARE_AT_END 1
