@@ -170,7 +170,11 @@ constexpr int kTraverseChunk = EMST_TRAV_CHUNK;   // consecutive Morton queries 
 constexpr int kSmemStack = EMST_SMEM_STACK;       // stack entries per lane kept in shared memory
 // refill when this many lanes are idle (or all are); measured best: 10 in 3D, 16 in 2D
 // (37M blobs 3D traversal 44.58 -> 44.27 ms at 10; 24M blobs 2D +0.4 ms at 10, so 2D keeps 16)
-template <int D> constexpr int kRefillIdle = D == 3 ? EMST_REFILL_IDLE3 : EMST_REFILL_IDLE;
+#ifndef EMST_REFILL_IDLE_S
+#define EMST_REFILL_IDLE_S 0   // round 1's kernel (0: as the others)
+#endif
+template <int D, bool kSingle> constexpr int kRefillIdle =
+    kSingle && EMST_REFILL_IDLE_S ? EMST_REFILL_IDLE_S : (D == 3 ? EMST_REFILL_IDLE3 : EMST_REFILL_IDLE);
 #ifndef EMST_REFRESH_BY_VISITS
 #define EMST_REFRESH_BY_VISITS 1
 #endif
@@ -441,7 +445,7 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       if (done) finalize();
       break;
     }
-    if (n_idle >= kRefillIdle<D>) {        // warp-uniform
+    if (n_idle >= kRefillIdle<D, kSingle>) {   // warp-uniform
       if (done) finalize();
       if (pool_next >= pool_end && !exhausted) {
         unsigned long long base = 0;
