@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -197,6 +198,11 @@ struct emst_context {
   long long n = 0;
   bool tree_valid = false;
   long long tree_token = 0;       // bumped by every build: names the tree the context holds
+  cudaEvent_t merge_end = nullptr;  // the last merge's end (trace: device idle time to the next round)
+  cudaEvent_t ev_counters = nullptr;   // the queued counter copy (read_counters_async)
+  size_t counters_timers = 0;          // timers recorded before it
+  std::function<void()> next_round;    // the solve's next round, first half, queued while the host waits
+  double gap_ms = 0.0;
   long long reuse_token = 0;      // set by emst_context_reuse_tree: the next building block may skip its build
   bool state_on_device = false;   // building-block arrays are device pointers (emst_context_set_state_on_device)
   // find_component_outgoing_edges keeps its nearest-foreign proofs for the next call on the
@@ -232,9 +238,12 @@ cudaEvent_t timer_event(emst_context* c) {
   return e;
 }
 
-// collect every recorded timer (call after a stream sync: all their events are complete)
-void timers_resolve(emst_context* c) {
-  for (const auto& t : c->timers) {
+// Collect the first `upto` recorded timers (all of them by default; their events
+// are complete).  The event pool is recycled only once no timer is pending.
+void timers_resolve(emst_context* c, size_t upto = (size_t)-1) {
+  upto = std::min(upto, c->timers.size());
+  for (size_t i = 0; i < upto; ++i) {
+    const auto& t = c->timers[i];
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, t.a, t.b));
     if (t.acc) *t.acc += ms;
@@ -243,19 +252,29 @@ void timers_resolve(emst_context* c) {
       if (c->trace) fprintf(stderr, "[emst] round %d traverse [%lld, %lld): %.3f ms\n", t.round, t.q0, t.q1, ms);
     }
   }
-  c->timers.clear();
-  c->ev_next = 0;
+  c->timers.erase(c->timers.begin(), c->timers.begin() + (long)upto);
+  if (c->timers.empty()) c->ev_next = 0;
 }
-
-void read_counters(emst_context* c) {
+// The counters read in two halves: queue the copy (and note the timers it
+// covers), then, after more work has been queued behind it, wait for it.
+void read_counters_async(emst_context* c) {
   CK(cudaMemcpyAsync(c->host_counters, c->counters.p, kCounters * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
-  CK(cudaStreamSynchronize(c->stream));
-  timers_resolve(c);
+  if (!c->ev_counters) CK(cudaEventCreateWithFlags(&c->ev_counters, cudaEventDisableTiming));
+  CK(cudaEventRecord(c->ev_counters, c->stream));
+  c->counters_timers = c->timers.size();
+}
+void read_counters_finish(emst_context* c) {
+  CK(cudaEventSynchronize(c->ev_counters));
+  timers_resolve(c, c->counters_timers);
   if (c->front_pending) {   // the labelling kernel's count of nodes still mixed
     c->front_n = (long long)(unsigned)c->host_counters[8];
     c->front_pending = false;
     if (c->trace) fprintf(stderr, "[emst] comps %lld: %lld nodes still mixed\n", c->round_comps, c->front_n);
   }
+}
+void read_counters(emst_context* c) {
+  read_counters_async(c);
+  read_counters_finish(c);
 }
 
 // ------------------------------------------------------------------- scan
@@ -586,9 +605,19 @@ void launch_labels(emst_context* c, long long n, LabelMode mode, bool want_top) 
 
 void allreduce_u64(emst_context* c, unsigned long long* buf, long long count, int rows, long long stride, bool sum);
 
-void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds,
-                   bool want_top = false, LabelMode mode = kLabelsFull) {
-  c->top_valid = false;
+// Phase 1 of a round, first half: the component bounds (boundary-pair and window
+// seeds) and the boundary prefix the labels need.  Uses the labels, c->round and
+// c->round_comps (an upper bound is enough: it only steers the window seeds).
+void prepare_bounds(emst_context* c, long long n, bool bounds, double* ms_bounds, LabelMode mode) {
+  if (c->trace && c->merge_end && c->round > 1) {
+    // (trace) the device's idle time from the last merge to this round's first kernel
+    CK(cudaEventSynchronize(c->merge_end));
+    cudaEvent_t now = timer_event(c);
+    CK(cudaEventSynchronize(now));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->merge_end, now));
+    c->gap_ms += ms;
+  }
   // Ranks of a multi-GPU solve (rounds >= 2) seed the bounds of their own Morton range only and
   // meet in one min-allreduce; round 1's streaming seeds and the building blocks stay replicated.
   const bool sharded = bounds && c->world > 1 && c->round > 1;
@@ -623,18 +652,36 @@ void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels,
     launch(c, kern, (unsigned)std::max<long long>(1, b1 - b0), kSeedThreads, 0, (const int*)c->label.p,
            (const float4*)c->spts.p, n, W, c->ub.p, b0);
   }
-  // the ranks' seeds meet in one min-allreduce of the c bounds (u64 bit patterns)
-  if (sharded) allreduce_u64(c, c->ub.p, c->round_comps, 1, 0, false);
+  c->timers.push_back({e0, timer_event(c), ms_bounds, false, c->round, 0, 0});
+}
+
+// The ranks' seeds meet in one min-allreduce of the c bounds (u64 bit patterns); needs
+// the exact component count.
+void exchange_bounds(emst_context* c, bool bounds, double* ms_bounds) {
+  if (!(bounds && c->world > 1 && c->round > 1)) return;
+  cudaEvent_t e0 = timer_event(c);
+  allreduce_u64(c, c->ub.p, c->round_comps, 1, 0, false);
+  c->timers.push_back({e0, timer_event(c), ms_bounds, false, c->round, 0, 0});
+}
+
+// Phase 1, second half: the node labels (needs the last labelling's count of mixed nodes).
+void prepare_labels(emst_context* c, long long n, double* ms_labels, bool want_top, LabelMode mode) {
+  c->top_valid = false;
   cudaEvent_t e1 = timer_event(c);
   if (n > 1 && mode != kLabelsNone) {
     if (c->dim == 3) launch_labels<Node3>(c, n, mode, want_top);
     else launch_labels<Node2>(c, n, mode, want_top);
     c->top_valid = want_top && mode == kLabelsFrontier;
   }
-  cudaEvent_t e2 = timer_event(c);
   // (no sync here: the times and the count of nodes still mixed are read at the round's counter read)
-  c->timers.push_back({e0, e1, ms_bounds, false, c->round, 0, 0});
-  c->timers.push_back({e1, e2, ms_labels, false, c->round, 0, 0});
+  c->timers.push_back({e1, timer_event(c), ms_labels, false, c->round, 0, 0});
+}
+
+void round_prepare(emst_context* c, long long n, bool bounds, double* ms_labels, double* ms_bounds,
+                   bool want_top = false, LabelMode mode = kLabelsFull) {
+  prepare_bounds(c, n, bounds, ms_bounds, mode);
+  exchange_bounds(c, bounds, ms_bounds);
+  prepare_labels(c, n, ms_labels, want_top, mode);
 }
 
 template <int D, bool S, bool B, bool M, bool P, bool G = false>
@@ -790,6 +837,9 @@ void round_find_all(emst_context* c, long long n, long long comps, int flags) {
 // singletons: the solve's round 1, where label[s] == s
 long long round_merge(emst_context* c, long long n, long long comps, long long edge_base, long long* emitted,
                       double* ms_merge = nullptr, bool singletons = false, const unsigned* iperm = nullptr) {
+  // (the solve's next-round work to queue behind the counter copy; consumed here, once)
+  std::function<void()> next_round = std::move(c->next_round);
+  c->next_round = nullptr;
   cudaEvent_t m0 = timer_event(c);
   int* err = reinterpret_cast<int*>(dev_counter(c, 2));
   launch(c, k_merge_succ, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, (const int*)c->label.p,
@@ -800,8 +850,11 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
            true);
   launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->root.p, (const int*)c->newid.p, comps, c->fin.p);
   launch(c, k_relabel, grid_for((n + 3) / 4, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
-  c->timers.push_back({m0, timer_event(c), ms_merge, false, c->round, 0, 0});
-  read_counters(c);   // (the round's one host sync; it also collects the round's timers)
+  c->merge_end = timer_event(c);
+  c->timers.push_back({m0, c->merge_end, ms_merge, false, c->round, 0, 0});
+  read_counters_async(c);
+  if (next_round) next_round();   // (work queued behind the counter copy, before the host waits)
+  read_counters_finish(c);   // (the round's one host sync; it also collects the round's timers)
   long long* h = c->host_counters;
   if (h[2] & kErrNoEdge) fail(EMST_ERR_NO_EDGE, "a component found no valid outgoing edge");
   if (h[2] & kErrChain) fail(EMST_ERR_CHAIN, "component chain did not terminate in a pair");
@@ -1015,11 +1068,24 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   long long visits_before = 0, found_before = 0, skipped_before = 0;
   double tv_before = c->traverse_ms;
   const bool bounds = flags & EMST_UPPER_BOUNDS;
+  const bool skip = flags & EMST_SUBTREE_SKIP;
+  // A round's bounds need only the relabelled components and an upper bound of
+  // their count (Boruvka at least halves it), so they are queued behind the
+  // merge's counter copy: the device computes them while the host waits for
+  // the counters, instead of idling between the rounds.
+  bool prepped = false;   // the bounds of round st->iterations + 1 are queued
+  auto queue_bounds = [&](int round, long long comps_bound, long long comps_guess) {
+    CK(cudaMemsetAsync(c->ub.p, 0xff, comps_bound * sizeof(unsigned long long), c->stream));
+    CK(cudaMemsetAsync(c->best.p, 0xff, comps_bound * sizeof(EdgeKey), c->stream));
+    c->round = round;
+    c->round_comps = comps_guess;   // (steers the window seeds only)
+    prepare_bounds(c, n, bounds, &ms_bounds, comps_bound == n ? kLabelsNone : skip ? kLabelsFrontier : kLabelsFull);
+  };
   while (comps > 1) {
     st->iterations++;
     if (st->iterations > max_it) fail(EMST_ERR_ITER, "exceeded the %d-iteration bound for n=%lld", max_it, n);
-    CK(cudaMemsetAsync(c->ub.p, 0xff, comps * sizeof(unsigned long long), c->stream));
-    CK(cudaMemsetAsync(c->best.p, 0xff, comps * sizeof(EdgeKey), c->stream));
+    if (!prepped) queue_bounds(st->iterations, comps, comps);
+    prepped = false;
     c->round = st->iterations;
     c->round_comps = comps;
     c->one_side = comps == 2 && c->last_round_one_side;
@@ -1031,9 +1097,9 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
       launch(c, k_pick_side, 1, 32, 0, (const unsigned long long*)dev_counter(c, 12), n, (int*)dev_counter(c, 13));
     }
     {
-      const bool skip = flags & EMST_SUBTREE_SKIP;
       const LabelMode mode = comps == n ? kLabelsNone : skip ? kLabelsFrontier : kLabelsFull;
-      round_prepare(c, n, bounds, &ms_labels, &ms_bounds, skip && comps < n, mode);
+      exchange_bounds(c, bounds, &ms_bounds);
+      prepare_labels(c, n, &ms_labels, skip && comps < n, mode);
     }
     cudaEvent_t f0 = timer_event(c);
     c->singleton_round = comps == n;
@@ -1043,7 +1109,14 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     c->round = 0;
     c->timers.push_back({f0, timer_event(c), &ms_find, false, st->iterations, 0, 0});
     long long emitted = 0;
+    const long long bound_next = comps / 2;   // (every component merges with at least one other)
+    const int it = st->iterations;
+    if (bound_next > 1 && it < max_it)
+      // (components shrink 3-4x per round: a quarter guesses the window-seed decision the exact
+      // count would make)
+      c->next_round = [&, it, bound_next] { queue_bounds(it + 1, bound_next, bound_next / 2); prepped = true; };
     long long next = round_merge(c, n, comps, edges, &emitted, &ms_merge, comps == n);
+    c->next_round = nullptr;
     if (st->iterations <= 64) {
       const int r = st->iterations - 1;
       st->round_traverse_ms[r] = c->traverse_ms - tv_before;
@@ -1083,6 +1156,9 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     evals = c->host_counters[0];
   }
   st->leaf_distance_evals = evals;
+  if (c->trace) fprintf(stderr, "[emst] merge-to-next-round gaps: %.3f ms in all\n", c->gap_ms);
+  c->gap_ms = 0.0;
+  c->merge_end = nullptr;
 #ifdef EMST_VISIT_HIST
   if (c->trace) visit_hist_print(c);
 #endif
