@@ -1156,7 +1156,12 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     evals = c->host_counters[0];
   }
   st->leaf_distance_evals = evals;
-  if (c->trace) fprintf(stderr, "[emst] merge-to-next-round gaps: %.3f ms in all\n", c->gap_ms);
+  if (c->trace) {
+    fprintf(stderr, "[emst] merge-to-next-round gaps: %.3f ms in all\n", c->gap_ms);
+    fprintf(stderr, "[emst] final order: longest equal-key run %u, runs of 33..4096: %u, runs of 9..32: %u\n",
+            (unsigned)(c->host_counters[7] & 0xffffffffll), (unsigned)((unsigned long long)c->host_counters[7] >> 32),
+            (unsigned)(c->host_counters[11] & 0xffffffffll));
+  }
   c->gap_ms = 0.0;
   c->merge_end = nullptr;
 #ifdef EMST_VISIT_HIST
