@@ -88,6 +88,7 @@ __device__ __forceinline__ unsigned long long seed_weight(const float* pa, const
 
 struct RoundScanOp {
   using T = unsigned;
+  static constexpr bool kCached = false;
   const int* label;
   const float4* spts;
   unsigned long long* ub;
@@ -555,6 +556,7 @@ __global__ void k_merge_jump(int* ptr, long long c, int* __restrict__ root, int*
 // gives every root its new dense id.
 struct MergeScanOp {
   using T = unsigned long long;
+  static constexpr bool kCached = true;   // the scan pass reads the flags the reduce pass cached
   __device__ void side(long long, int, const unsigned long long*) const {}
   const int* succ;
   const int* root;
@@ -562,6 +564,29 @@ struct MergeScanOp {
   EdgeKey* eout;   // emitted edges (u << 32 | v, weight bits), one 16-byte record each
   long long edge_base;
   int* newid;
+  unsigned char* cache;   // one byte of flags per component (bit 0 edge, bit 1 root), 8-aligned runs
+  // The flags need a random read (succ[succ[k]]); the reduce pass caches them so
+  // that the scan pass reads 1 coalesced byte per component instead.
+  __device__ void put(long long i0, int cnt, const unsigned long long* v) const {
+    unsigned long long b = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j)
+      if (j < cnt) b |= (unsigned long long)((v[j] & 1ull) | ((v[j] >> 30) & 2ull)) << (8 * j);
+    if (cnt == kScanItems) *reinterpret_cast<unsigned long long*>(cache + i0) = b;
+    else
+      for (int j = 0; j < cnt; ++j) cache[i0 + j] = (unsigned char)(b >> (8 * j));
+  }
+  __device__ void get(long long i0, int cnt, unsigned long long* v) const {
+    unsigned long long b = 0;
+    if (cnt == kScanItems) b = *reinterpret_cast<const unsigned long long*>(cache + i0);
+    else
+      for (int j = 0; j < cnt; ++j) b |= (unsigned long long)cache[i0 + j] << (8 * j);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      const unsigned long long f = (b >> (8 * j)) & 3ull;
+      v[j] = j < cnt ? ((f & 1ull) | ((f >> 1) << 31)) : 0ull;
+    }
+  }
   __device__ void load(long long i0, int cnt, unsigned long long* v) const {
     int y[kScanItems], r[kScanItems], yy[kScanItems];
     load8(succ, i0, cnt, y);

@@ -846,7 +846,9 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
          iperm ? iperm : (const unsigned*)c->iperm.p, c->succ.p, err, singletons);
   launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
   launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, c->root.p, err);
-  run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->eout.p, edge_base, c->newid.p},
+  // (the flag cache borrows fin, which k_merge_final writes after the scan)
+  run_scan(c, comps, MergeScanOp{c->succ.p, c->root.p, c->best.p, c->eout.p, edge_base, c->newid.p,
+                                 reinterpret_cast<unsigned char*>(c->fin.p)},
            true);
   launch(c, k_merge_final, grid_for(comps, 256), 256, 0, (const int*)c->root.p, (const int*)c->newid.p, comps, c->fin.p);
   launch(c, k_relabel, grid_for((n + 3) / 4, 256), 256, 0, c->label.p, (const int*)c->fin.p, n);
@@ -2063,6 +2065,7 @@ __global__ void k_edges_out(const EdgeKey* __restrict__ eout, long long ne, long
 // new_reps: the representatives that are their cluster's minimum, in k (= ascending) order
 struct NewRepsOp {
   using T = unsigned;
+  static constexpr bool kCached = false;
   const int* root;
   const long long* reps;
   const long long* cmin;

@@ -181,6 +181,7 @@ k_scan(long long n, long long seg, unsigned long long* status, Op op, unsigned l
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) v[j] = T(0);
     op.load(i0, cnt, v);
+    if constexpr (Op::kCached) { if (cnt > 0) op.put(i0, cnt, v); }
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) acc += v[j];
   }
@@ -196,7 +197,8 @@ k_scan(long long n, long long seg, unsigned long long* status, Op op, unsigned l
     T v[kScanItems];
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) v[j] = T(0);
-    op.load(i0, cnt, v);
+    if constexpr (Op::kCached) { if (cnt > 0) op.get(i0, cnt, v); }
+    else op.load(i0, cnt, v);
     T mine = T(0);
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) mine += v[j];
