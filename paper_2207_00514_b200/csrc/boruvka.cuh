@@ -199,6 +199,41 @@ __global__ void __launch_bounds__(kScanThreads) k_seed_boundary(const int* __res
   apply_bound_updates<2 * kScanItems>(ul, uw, ub);   // every lane of the warp takes part
 }
 
+// Round 1 with a wider Z-window: ub[s] = the smallest upper bound of |s - t| over
+// the slots t within +-W of s (singletons: no labels, no atomics).  The points of
+// a block and its halo are staged in shared memory.
+constexpr int kSeed1Threads = 256;
+template <int D, int W>
+__global__ void __launch_bounds__(kSeed1Threads) k_seed_round1_window(const float4* __restrict__ spts, long long n,
+                                                                      unsigned long long* __restrict__ ub) {
+  __shared__ float4 sp[kSeed1Threads + 2 * W];
+  const long long base = blockIdx.x * (long long)kSeed1Threads;
+  for (int i = threadIdx.x; i < kSeed1Threads + 2 * W; i += kSeed1Threads) {
+    const long long g = base - W + i;
+    sp[i] = g >= 0 && g < n ? spts[g] : make_float4(__int_as_float(0x7f800000), 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
+  const long long s = base + threadIdx.x;
+  if (s >= n) return;
+  const float4 a = sp[threadIdx.x + W];
+  const float pa[3] = {a.x, a.y, a.z};
+  float best = __int_as_float(0x7f800000);
+#pragma unroll
+  for (int k = 1; k <= W; ++k) {
+#pragma unroll
+    for (int sgn = -1; sgn <= 1; sgn += 2) {
+      const float4 b = sp[threadIdx.x + W + sgn * k];
+      if (b.x < __int_as_float(0x7f800000)) {
+        const float pb[3] = {b.x, b.y, b.z};
+        best = fminf(best, point_ub2<D>(pa, pb));
+      }
+    }
+  }
+  ub[s] = best < __int_as_float(0x7f800000)
+              ? (unsigned long long)__double_as_longlong(__dmul_ru((double)__fsqrt_ru(best), 1.0 + 0x1p-40))
+              : ~0ull;
+}
+
 // Round 1 of the solve: every slot is its own component (labels are the slot
 // ids), so the boundary-pair fold of the round scan reduces to
 // ub[s] = min(w(s-1, s), w(s, s+1)) (mst.py:198-224; f32 upper bounds of the weights, seed_weight):
