@@ -178,6 +178,9 @@ template <int D, bool kSingle> constexpr int kRefillIdle =
 #ifndef EMST_REFRESH_BY_VISITS
 #define EMST_REFRESH_BY_VISITS 1
 #endif
+#ifndef EMST_STACK_FAST
+#define EMST_STACK_FAST 1   // pushes branch once on "all in shared memory" (1); pops and single pushes too (2)
+#endif
 #ifndef EMST_RADIUS_REFRESH
 #define EMST_RADIUS_REFRESH 4096
 #endif
@@ -583,7 +586,14 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     // Parked entries the radius has since pruned are dropped first.
     int2 e = make_int2(-1, 0);
     while (top > 0) {
+#if EMST_STACK_FAST >= 2
+      if (top <= kSmemStack)
+        asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(e.x), "=r"(e.y) : "r"(stk0 + (top - 1) * kStkStride));
+      else
+        e = deep[top - 1 - kSmemStack];
+#else
       e = stk_get(top - 1);
+#endif
       if (__int_as_float(e.y) <= r2) break;
       if (kProof) pmin2 = fminf(pmin2, __int_as_float(e.y));
       --top;
@@ -635,10 +645,28 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       } else if (np == 2) {
         // nearer child on top (popped first); ties keep the left child there
         const bool near1 = lb1 < lb0;
+#if EMST_STACK_FAST
+        if (top + 2 <= kSmemStack) {   // (the common case: both entries in shared memory, one branch)
+          asm volatile("st.shared.v2.s32 [%0], {%1, %2};" :: "r"(stk0 + top * kStkStride),
+                       "r"(near1 ? rec.ref.x : rec.ref.y), "r"(__float_as_int(near1 ? lb0 : lb1)) : "memory");
+          asm volatile("st.shared.v2.s32 [%0], {%1, %2};" :: "r"(stk0 + (top + 1) * kStkStride),
+                       "r"(near1 ? rec.ref.y : rec.ref.x), "r"(__float_as_int(near1 ? lb1 : lb0)) : "memory");
+        } else {
+          stk_put(top, near1 ? rec.ref.x : rec.ref.y, near1 ? lb0 : lb1);
+          stk_put(top + 1, near1 ? rec.ref.y : rec.ref.x, near1 ? lb1 : lb0);
+        }
+#else
         stk_put(top, near1 ? rec.ref.x : rec.ref.y, near1 ? lb0 : lb1);
         stk_put(top + 1, near1 ? rec.ref.y : rec.ref.x, near1 ? lb1 : lb0);
+#endif
         top += 2;
       } else if (np == 1) {
+#if EMST_STACK_FAST >= 2
+        if (top < kSmemStack)
+          asm volatile("st.shared.v2.s32 [%0], {%1, %2};" :: "r"(stk0 + top * kStkStride),
+                       "r"(want0 ? rec.ref.x : rec.ref.y), "r"(__float_as_int(want0 ? lb0 : lb1)) : "memory");
+        else
+#endif
         stk_put(top, want0 ? rec.ref.x : rec.ref.y, want0 ? lb0 : lb1);
         ++top;
       }
