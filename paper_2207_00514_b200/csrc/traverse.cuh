@@ -178,6 +178,9 @@ template <int D, bool kSingle> constexpr int kRefillIdle =
 #ifndef EMST_REFRESH_BY_VISITS
 #define EMST_REFRESH_BY_VISITS 1
 #endif
+#ifndef EMST_DONE_PREFETCH
+#define EMST_DONE_PREFETCH 0   // L1 prefetch of the candidate point when a query ends (measured: off is 0.1-0.5 ms faster)
+#endif
 #ifndef EMST_STACK_FAST
 #define EMST_STACK_FAST 1   // pushes branch once on "all in shared memory" (1); pops and single pushes too (2)
 #endif
@@ -569,7 +572,9 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
     }
     if (s < 0 || done) continue;
 
-#if EMST_REFRESH_BY_VISITS
+#if EMST_RADIUS_REFRESH == 0
+    if (false) {   // (no refresh: the staged radius stands for the whole search)
+#elif EMST_REFRESH_BY_VISITS
     // (the lane's visit counter doubles as the refresh clock: one increment per step less)
     if (kBounds && !(kSingle || singletons) && (visits & (kRadiusRefresh - 1)) == kRadiusRefresh - 1) {
 #else
@@ -689,7 +694,9 @@ k_traverse(const typename NodeOf<D>::type* __restrict__ nodes, const float4* __r
       done = true;
       // finalize() reads the candidate's point at the next refill: start the
       // fetch now so that it is an L1 hit by then
+#if EMST_DONE_PREFETCH
       if (pend.slot >= 0) asm volatile("prefetch.global.L1 [%0];" :: "l"(spts + pend.slot));
+#endif
     }
   }
   unsigned long long ev64 = evals, vi64 = visits, fo64 = found, sk64 = skipped;
