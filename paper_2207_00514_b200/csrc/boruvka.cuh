@@ -269,7 +269,7 @@ __global__ void k_seed_round1(const float4* __restrict__ spts, long long n, cons
 // outgoing edge, so its weight may lower both components' radii; only an upper
 // bound is needed, so it is f32 rounded up (+2^-40 slack) -- no
 // f64.  A block stages its slots [base, base+T) and W on either side (labels,
-// points) in shared memory once.  Each pair (i, i+k), k = 2..W, is computed
+// points) in shared memory once.  Each pair (i, i+k), k = 1..W, is computed
 // once, by the thread of its lower slot (including the W slots left of the
 // block): the lower end keeps a register minimum, the upper end gets a
 // shared-memory atomic min (squared f32 bounds >= 0 order as their bits).
@@ -286,7 +286,7 @@ __device__ __forceinline__ float seed_pairs(const float4* sp, const int* sl, uns
   const float q[3] = {pa.x, pa.y, pa.z};
   const int kmax = kW ? kW : W;
 #pragma unroll
-  for (int k = 2; k <= (kW ? kW : kSeedMaxW); ++k) {
+  for (int k = 1; k <= (kW ? kW : kSeedMaxW); ++k) {   // (k = 1: the boundary pairs; the scan then skips them)
     if (!kW && k > kmax) break;
     const int b = a + k;
     if (b >= lim) break;
@@ -475,15 +475,37 @@ __global__ void __launch_bounds__(kScanThreads) k_prefilter(const float4* __rest
   for (long long t0 = q0 + (long long)blockIdx.x * kScanTile; t0 < q1; t0 += (long long)gridDim.x * kScanTile) {
     const long long i0 = t0 + (long long)threadIdx.x * kScanItems;
     unsigned keep = 0;   // bit j: slot i0 + j is listed
+    // the thread's 8 labels, proofs and top pure nodes in 16-byte loads (a
+    // shard range may start off the 8-slot grid: those tiles load per slot)
+    const int cnt = i0 >= q1 ? 0 : (q1 - i0 < kScanItems ? (int)(q1 - i0) : kScanItems);
+    const int vcnt = (i0 & (kScanItems - 1)) ? -1 : cnt;
+    int labs[kScanItems], tops[kScanItems];
+    float lbs[kScanItems];
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) { labs[j] = 0; tops[j] = 0; lbs[j] = 0.f; }
+    if (vcnt >= 0) {
+      load8(label, i0, vcnt, labs);
+      load8(nfn_lb, i0, vcnt, lbs);
+      if (top) load8(top, i0, vcnt, tops);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kScanItems; ++j)
+        if (j < cnt) { labs[j] = label[i0 + j]; lbs[j] = nfn_lb[i0 + j]; tops[j] = top ? top[i0 + j] : 0; }
+    }
+    // (the bounds are final here: read through L1, once per run of equal labels)
+    int plab = -1;
+    double prad = 0.0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
       const long long s = i0 + j;
-      if (s >= q1) break;
-      const int comp = label[s];
-      const double radius = bits_to_radius(__ldcg(&ub[comp]));
-      bool k = !((double)nfn_lb[s] > radius) && comp != skip_comp;
+      if (j >= cnt) break;
+      const int comp = labs[j];
+      const double radius = comp == plab ? prad : bits_to_radius(__ldg(&ub[comp]));
+      plab = comp;
+      prad = radius;
+      bool k = !((double)lbs[j] > radius) && comp != skip_comp;
       if (k && top) {
-        const int t = top[s];
+        const int t = tops[j];
         if (t > 0) {
           const int2 ut = __ldg(up + (t - 1));
           if (ut.x < 0) {

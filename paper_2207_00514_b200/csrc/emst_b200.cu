@@ -113,7 +113,7 @@ struct emst_context {
   int device = 0, rank = 0, world = 1, vshards = 1;
   bool singleton_round = false;   // every component is one point (round 1 of a solve)
   int round = 0;                  // 1-based Boruvka round of the running solve (0 outside)
-  int seed_window = 8;            // extra Z-order seed pairs (s +- 2..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
+  int seed_window = 8;            // Z-order seed pairs (s +- 1..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
   long long round_comps = 0;      // components entering the running round
   int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
   double skip_frac = 0.0;         // share of last round's queries settled before their first visit
@@ -625,6 +625,10 @@ void prepare_bounds(emst_context* c, long long n, bool bounds, double* ms_bounds
   // meet in one min-allreduce; round 1's streaming seeds and the building blocks stay replicated.
   const bool sharded = bounds && c->world > 1 && c->round > 1;
   const long long r0 = sharded ? c->rank * n / c->world : 0, r1 = sharded ? (c->rank + 1) * n / c->world : n;
+  // window seeds pay while components are small and in 3D (measured: 37M blobs 3D
+  // -2.3 ms, 10M normal 3D -0.6 ms; the 2D configs lose ~1 %); later rounds gain nothing
+  const bool window = bounds && c->seed_window > 1 && c->dim == 3 && c->round >= c->seed_from && !c->core &&
+                      c->round_comps * 1024 >= n;
   cudaEvent_t e0 = timer_event(c);
   if (mode == kLabelsNone && c->round == 1) {
     // round 1 of the solve: singletons, no node labels, so no boundary prefix either
@@ -641,18 +645,18 @@ void prepare_bounds(emst_context* c, long long n, bool bounds, double* ms_bounds
     // ranks of a multi-GPU solve seed only their own Morton range (below), so the scan then
     // just counts the boundaries
     // (exact weights for the building block compute_upper_bounds, round 0; upper bounds in the solve)
-    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds && !sharded, c->core,
-                               c->round == 0},
+    // (the window's pairs include every boundary pair (s, s + 1): with the window on, the
+    // scan only counts the boundaries)
+    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim,
+                               bounds && !sharded && !window, c->core, c->round == 0},
              false);
   }
-  if (sharded && r1 > r0) {
+  if (sharded && !window && r1 > r0) {
     const unsigned g = grid_for((r1 - r0 + kScanItems - 1) / kScanItems, kScanThreads);
     if (c->dim == 3) launch(c, k_seed_boundary<3>, g, kScanThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, r0, r1, c->core, c->ub.p);
     else launch(c, k_seed_boundary<2>, g, kScanThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, r0, r1, c->core, c->ub.p);
   }
-  // window seeds pay while components are small and in 3D (measured: 37M blobs 3D
-  // -2.3 ms, 10M normal 3D -0.6 ms; the 2D configs lose ~1 %); later rounds gain nothing
-  if (bounds && c->seed_window > 1 && c->dim == 3 && c->round >= c->seed_from && !c->core && c->round_comps * 1024 >= n) {
+  if (window) {
     const int W = std::min(c->seed_window, kSeedMaxW);
     const auto kern = c->dim == 3 ? (W == 8 ? k_seed_window<3, 8> : k_seed_window<3, 0>)
                                   : (W == 8 ? k_seed_window<2, 8> : k_seed_window<2, 0>);
@@ -726,7 +730,10 @@ void traverse_range_m(emst_context* c, EdgeKey* out, long long q0, long long q1)
   if (use_list) {
     c->qlist.ensure(q1 - q0);
     CK(cudaMemsetAsync(qcount, 0, sizeof(long long), c->stream));
-    const unsigned pg = (unsigned)std::min<long long>(grid_for(q1 - q0, kScanTile), (long long)c->num_sms * 8);
+    static int pf_per_sm[4] = {0, 0, 0, 0};   // resident blocks per SM (one wave, no tail)
+    if (!pf_per_sm[D]) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&pf_per_sm[D], k_prefilter<D>, kScanThreads, 0));
+    const unsigned pg = (unsigned)std::min<long long>(grid_for(q1 - q0, kScanTile),
+                                                      (long long)c->num_sms * std::max(pf_per_sm[D], 1));
     launch(c, k_prefilter<D>, pg, kScanThreads, 0, (const float4*)c->spts.p, (const int*)c->label.p,
            (const unsigned long long*)c->ub.p, (const float*)c->nfn_lb.p,
            c->top_valid ? (const int*)c->top.p : (const int*)nullptr, (const int2*)c->up.p, (const Scene*)c->scene.p,
