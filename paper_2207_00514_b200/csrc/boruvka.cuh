@@ -809,10 +809,8 @@ __global__ void k_edge_ties(const unsigned* __restrict__ key, long long ne, cons
       len = (int)(lo - i + 1);
     }
   }
-  if (len == 2) {
-    const unsigned o0 = order[i], o1 = order[i + 1];
-    if (wuv_less(eout[o1], eout[o0])) { order[i] = o1; order[i + 1] = o0; }
-  } else if (len > 2 && len <= kThreadTie) {
+  // (a run of exactly two is ordered by the emit itself, which gathers both records anyway)
+  if (len > 2 && len <= kThreadTie) {
     // in registers: all loads issued at once, then a fixed compare-exchange network
     unsigned o[kThreadTie];
     EdgeKey k[kThreadTie];
@@ -944,22 +942,60 @@ __global__ void k_edge_w_keys(const EdgeKey* __restrict__ eout, const unsigned* 
   if (i < ne) keys[i] = eout[order[i]].w;
 }
 
+// The record at final position i.  With the sorted 32-bit keys given, a run of
+// exactly two equal keys (the common tie or collision, left alone by
+// k_edge_ties) is put in exact (w, uv) order here: its first position takes the
+// smaller of the two records, its second the larger (the partner's record by
+// shuffle, or loaded at a warp edge).  All lanes of the warp must call it.
+__device__ __forceinline__ EdgeKey final_record(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout,
+                                                const unsigned* __restrict__ key, long long ne, long long i) {
+  const bool valid = i < ne;
+  EdgeKey e;
+  e.w = ~0ull;
+  e.uv = ~0ull;
+  if (valid) e = eout[order[i]];
+  if (!key) return e;   // (grid-uniform: the exact fallback's order has no ties left)
+  int side = 0;         // +1: first of a two-run, -1: its second
+  if (valid) {
+    const unsigned k0 = key[i];
+    const bool eqn = i + 1 < ne && key[i + 1] == k0, eqp = i > 0 && key[i - 1] == k0;
+    if (eqn && !eqp && !(i + 2 < ne && key[i + 2] == k0)) side = 1;
+    else if (eqp && !eqn && !(i > 1 && key[i - 2] == k0)) side = -1;
+  }
+  const unsigned lane = threadIdx.x & 31u;
+  EdgeKey up, dn;   // the records of lanes + 1 and - 1
+  up.w = __shfl_down_sync(0xffffffffu, e.w, 1);
+  up.uv = __shfl_down_sync(0xffffffffu, e.uv, 1);
+  dn.w = __shfl_up_sync(0xffffffffu, e.w, 1);
+  dn.uv = __shfl_up_sync(0xffffffffu, e.uv, 1);
+  if (side == 1) {
+    const EdgeKey p = lane == 31 ? eout[order[i + 1]] : up;
+    if (wuv_less(p, e)) e = p;
+  } else if (side == -1) {
+    const EdgeKey p = lane == 0 ? eout[order[i - 1]] : dn;
+    if (wuv_less(e, p)) e = p;
+  }
+  return e;
+}
+
 // edge order -> the reference's int64 (u, v) rows and f64 weights
-__global__ void k_edge_emit(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout, long long ne,
-                            long long* __restrict__ edges, double* __restrict__ weights) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+__global__ void k_edge_emit(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout,
+                            const unsigned* __restrict__ key, long long ne, long long* __restrict__ edges,
+                            double* __restrict__ weights) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const EdgeKey e = final_record(order, eout, key, ne, i);
   if (i >= ne) return;
-  const EdgeKey e = eout[order[i]];
   reinterpret_cast<longlong2*>(edges)[i] = make_longlong2((long long)(e.uv >> 32), (long long)(e.uv & 0xffffffffull));
   weights[i] = __longlong_as_double((long long)e.w);
 }
 
 // the host-pointer entry's variant: packed (u << 32 | v) rows, 8 bytes per edge over PCIe (hostio.h)
-__global__ void k_edge_emit_packed(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout, long long ne,
+__global__ void k_edge_emit_packed(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout,
+                                   const unsigned* __restrict__ key, long long ne,
                                    unsigned long long* __restrict__ packed, double* __restrict__ weights) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const EdgeKey e = final_record(order, eout, key, ne, i);
   if (i >= ne) return;
-  const EdgeKey e = eout[order[i]];
   packed[i] = e.uv;
   weights[i] = __longlong_as_double((long long)e.w);
 }

@@ -887,12 +887,14 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
 // run counts from the device: no host sync).  A run longer than kBlockTie
 // (checked by the caller at the solve's final counter read, sort_overflowed)
 // is redone by sort_and_emit_exact.
-void emit_edges(emst_context* c, const unsigned* order, long long ne, long long* edges_dst, double* w_dst, bool packed) {
+// (key: the sorted 32-bit keys, whose two-runs the emit orders; nullptr: order is final)
+void emit_edges(emst_context* c, const unsigned* order, const unsigned* key, long long ne, long long* edges_dst,
+                double* w_dst, bool packed) {
   if (packed)
-    launch(c, k_edge_emit_packed, grid_for(ne, 256), 256, 0, order, (const EdgeKey*)c->eout.p, ne,
+    launch(c, k_edge_emit_packed, grid_for(ne, 256), 256, 0, order, (const EdgeKey*)c->eout.p, key, ne,
            reinterpret_cast<unsigned long long*>(edges_dst), w_dst);
   else
-    launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, order, (const EdgeKey*)c->eout.p, ne, edges_dst, w_dst);
+    launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, order, (const EdgeKey*)c->eout.p, key, ne, edges_dst, w_dst);
 }
 
 void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* w_dst, bool packed = false) {
@@ -930,7 +932,7 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
   CK(cudaFuncSetAttribute(k_edge_fix_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEdgeFixSmem));
   launch(c, k_edge_fix_long, (unsigned)c->num_sms, 1024, kEdgeFixSmem, (const int2*)c->tie_runs.p,
          (const unsigned*)tie + 1, (const EdgeKey*)c->eout.p, order);
-  emit_edges(c, order, ne, edges_dst, w_dst, packed);
+  emit_edges(c, order, kin, ne, edges_dst, w_dst, packed);
 }
 
 // true when sort_and_emit met a tie run longer than kBlockTie (after a counter read)
@@ -950,7 +952,7 @@ void sort_and_emit_exact(emst_context* c, long long ne, long long* edges_dst, do
   unsigned long long* keys2;
   unsigned* order2;
   radix_sort(c, ne, 64, kin, order, false, keys, vin_alt, &keys2, &order2);
-  emit_edges(c, order2, ne, edges_dst, w_dst, packed);
+  emit_edges(c, order2, nullptr, ne, edges_dst, w_dst, packed);
 }
 
 // float(np.sum(weights)) on the device in numpy's summation order.
