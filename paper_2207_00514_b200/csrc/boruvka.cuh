@@ -89,6 +89,7 @@ __device__ __forceinline__ unsigned long long seed_weight(const float* pa, const
 struct RoundScanOp {
   using T = unsigned;
   static constexpr bool kCached = false;
+  static constexpr bool kWarpStore = false;
   const int* label;
   const float4* spts;
   unsigned long long* ub;
@@ -660,18 +661,36 @@ struct MergeScanOp {
       v[j] = edge | (is_root << 31);
     }
   }
+  // Called by every thread (cnt may be 0).  The edge records move warp-striped:
+  // each thread parks its 8 output positions in shared memory, then lane l
+  // copies items l, l + 32, ... of the warp's 256, so a warp's 16-byte reads of
+  // best and writes to eout are contiguous instead of 128 bytes apart.
+  static constexpr bool kWarpStore = true;
   __device__ void store(long long i0, int cnt, const unsigned long long* v, unsigned long long ex) const {
+    __shared__ int4 s_pos4[kScanThreads * kScanItems / 4];
+    int pos[kScanItems];
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
+      pos[j] = -1;
       if (j >= cnt) continue;
-      const long long k = i0 + j;
-      if (v[j] & 1ull) {
-        const long long at = edge_base + (long long)(ex & 0x7fffffffull);
-        eout[at] = best[k];
-      }
-      if (v[j] >> 31) newid[k] = (int)(ex >> 31);
+      if (v[j] & 1ull) pos[j] = (int)(ex & 0x7fffffffull);
+      if (v[j] >> 31) newid[i0 + j] = (int)(ex >> 31);
       ex += v[j];
     }
+    const unsigned lane = threadIdx.x & 31u;
+    int4* mine = s_pos4 + threadIdx.x * (kScanItems / 4);
+    mine[0] = make_int4(pos[0], pos[1], pos[2], pos[3]);
+    mine[1] = make_int4(pos[4], pos[5], pos[6], pos[7]);
+    __syncwarp();
+    const int* wpos = reinterpret_cast<const int*>(s_pos4) + (threadIdx.x - lane) * kScanItems;
+    const long long w0 = i0 - (long long)lane * kScanItems;   // the warp's first item
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+      const int idx = j * 32 + (int)lane;
+      const int at = wpos[idx];
+      if (at >= 0) eout[edge_base + at] = best[w0 + idx];
+    }
+    __syncwarp();   // (the positions are rewritten by the next tile)
   }
 };
 

@@ -2083,6 +2083,7 @@ __global__ void k_edges_out(const EdgeKey* __restrict__ eout, long long ne, long
 struct NewRepsOp {
   using T = unsigned;
   static constexpr bool kCached = false;
+  static constexpr bool kWarpStore = false;
   const int* root;
   const long long* reps;
   const long long* cmin;

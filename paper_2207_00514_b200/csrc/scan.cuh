@@ -15,7 +15,8 @@
 //                              after the tile's prefix is published (so the
 //                              look-back chain of the tiles behind never waits
 //                              on it); called by every thread
-//   op.store(i0, cnt, v, ex)   ex = exclusive prefix of item i0
+//   op.store(i0, cnt, v, ex)   ex = exclusive prefix of item i0 (threads with cnt 0
+//                              call it too when Op::kWarpStore)
 // Value arithmetic wraps (mod 2^32 for u32, mod 2^62 for u64), which is exact
 // whenever every true prefix fits, so signed contributions are allowed.
 #pragma once
@@ -205,7 +206,8 @@ k_scan(long long n, long long seg, unsigned long long* status, Op op, unsigned l
     T tile_total;
     const T off = block_exclusive<T>(mine, &tile_total);
     op.side(i0, cnt, v);
-    if (cnt > 0) op.store(i0, cnt, v, run + off);
+    if constexpr (Op::kWarpStore) op.store(i0, cnt, v, run + off);   // (every thread)
+    else if (cnt > 0) op.store(i0, cnt, v, run + off);
     run += tile_total;
   }
   if (total_out && threadIdx.x == 0 && s1 >= n && s0 < n) *total_out = (unsigned long long)seg_total;
