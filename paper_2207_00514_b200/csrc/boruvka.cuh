@@ -564,15 +564,24 @@ constexpr int kErrNoEdge = 1;     // mst.py:365-376 / 720-721
 constexpr int kErrChain = 2;      // mst.py:399-400 / 722-723
 
 __global__ void k_merge_succ(const EdgeKey* __restrict__ best, long long c, const int* __restrict__ label,
-                             const unsigned* __restrict__ iperm, int* __restrict__ succ, int* __restrict__ err,
-                             bool singletons) {
+                             const unsigned* __restrict__ perm, const unsigned* __restrict__ iperm,
+                             int* __restrict__ succ, int* __restrict__ err, bool singletons) {
   long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (k >= c) return;
   EdgeKey e = best[k];
   if (e.uv == ~0ull) { atomicOr(err, kErrNoEdge); succ[k] = (int)k; return; }
   unsigned u = (unsigned)(e.uv >> 32), v = (unsigned)(e.uv & 0xffffffffu);
-  // (round 1: every slot is its own component, label[s] == s)
-  const int su = (int)iperm[u], sv = (int)iperm[v];
+  int su, sv;
+  if (singletons) {
+    // round 1: every slot is its own component (label[s] == s) and one end of
+    // its edge is its own point perm[k]: only the other end is looked up
+    const unsigned pk = perm[k];
+    su = u == pk ? (int)k : (int)iperm[u];
+    sv = v == pk ? (int)k : (int)iperm[v];
+  } else {
+    su = (int)iperm[u];
+    sv = (int)iperm[v];
+  }
   int lu = singletons ? su : label[su], lv = singletons ? sv : label[sv];
   if (lu == (int)k && lv != (int)k) succ[k] = lv;
   else if (lv == (int)k && lu != (int)k) succ[k] = lu;

@@ -857,8 +857,10 @@ long long round_merge(emst_context* c, long long n, long long comps, long long e
   c->next_round = nullptr;
   cudaEvent_t m0 = timer_event(c);
   int* err = reinterpret_cast<int*>(dev_counter(c, 2));
+  // (an explicit iperm is the identity, its own inverse)
   launch(c, k_merge_succ, grid_for(comps, 256), 256, 0, (const EdgeKey*)c->best.p, comps, (const int*)c->label.p,
-         iperm ? iperm : (const unsigned*)c->iperm.p, c->succ.p, err, singletons);
+         iperm ? iperm : (const unsigned*)c->perm.p, iperm ? iperm : (const unsigned*)c->iperm.p, c->succ.p, err,
+         singletons);
   launch(c, k_merge_link, grid_for(comps, 256), 256, 0, (const int*)c->succ.p, comps, c->ptr.p);
   launch(c, k_merge_jump, grid_for(comps, 256), 256, 0, c->ptr.p, comps, c->root.p, err);
   // (the flag cache borrows fin, which k_merge_final writes after the scan)
