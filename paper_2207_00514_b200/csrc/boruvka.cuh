@@ -99,6 +99,10 @@ struct RoundScanOp {
   bool bounds;
   const double* core;   // mutual reachability (slot order), or nullptr
   bool exact;           // exact f64 weights (the building block) or upper bounds (the solve)
+  // the boundary pairs (s, s + 1) seeded: left slot s in [seed0, seed1) -- a rank of a
+  // multi-GPU solve seeds its own Morton range (the ranges tile [0, n - 1), so the
+  // min-allreduce of the bounds that follows gives every rank the replicated result)
+  long long seed0, seed1;
   __device__ void load(long long i0, int cnt, unsigned* v) const {
     int lab[kScanItems + 1];
 #pragma unroll
@@ -120,7 +124,7 @@ struct RoundScanOp {
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
       wb[j] = ~0ull;
-      if (v[j]) {
+      if (v[j] && i0 + j >= seed0 && i0 + j < seed1) {
         const float4 a = __ldg(spts + i0 + j), b = __ldg(spts + i0 + j + 1);
         const float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
         wb[j] = dim == 3 ? seed_weight<3>(pa, pb, exact) : seed_weight<2>(pa, pb, exact);
@@ -157,48 +161,6 @@ struct RoundScanOp {
     store8(bprefix, i0, cnt, out);
   }
 };
-
-// The boundary-pair seeds of RoundScanOp::side for the pairs (s, s + 1) whose left
-// slot s lies in [q0, q1): a rank of a multi-GPU solve seeds only its own Morton
-// range (the ranges tile [0, n - 1), so the min-allreduce of the bounds that
-// follows gives every rank the replicated result).  8 slots per thread.
-template <int D>
-__global__ void __launch_bounds__(kScanThreads) k_seed_boundary(const int* __restrict__ label,
-                                                                const float4* __restrict__ spts, long long n,
-                                                                long long q0, long long q1,
-                                                                const double* __restrict__ core,
-                                                                unsigned long long* ub) {
-  const long long i0 = q0 + (blockIdx.x * (long long)blockDim.x + threadIdx.x) * kScanItems;
-  const int cnt = i0 >= q1 ? 0 : (int)min((long long)kScanItems, q1 - i0);
-  int lab[kScanItems + 1];
-#pragma unroll
-  for (int j = 0; j <= kScanItems; ++j) lab[j] = j <= cnt && i0 + j < n ? label[i0 + j] : -1;
-  unsigned long long wb[kScanItems];
-  bool v[kScanItems];
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    v[j] = j < cnt && i0 + j + 1 < n && lab[j] != lab[j + 1];
-    wb[j] = ~0ull;
-    if (v[j]) {
-      const float4 a = __ldg(spts + i0 + j), b = __ldg(spts + i0 + j + 1);
-      const float pa[3] = {a.x, a.y, a.z}, pb[3] = {b.x, b.y, b.z};
-      double w = __longlong_as_double((long long)seed_weight<D>(pa, pb, false));
-      if (core) w = fmax(w, fmax(core[i0 + j], core[i0 + j + 1]));   // mst.py:217-220
-      wb[j] = (unsigned long long)__double_as_longlong(w);
-    }
-  }
-  // one update per label among the thread's pairs: both ends of every boundary pair
-  int ul[2 * kScanItems];
-  unsigned long long uw[2 * kScanItems];
-#pragma unroll
-  for (int j = 0; j < kScanItems; ++j) {
-    ul[2 * j] = v[j] ? lab[j] : -1;
-    uw[2 * j] = wb[j];
-    ul[2 * j + 1] = v[j] ? lab[j + 1] : -1;
-    uw[2 * j + 1] = wb[j];
-  }
-  apply_bound_updates<2 * kScanItems>(ul, uw, ub);   // every lane of the warp takes part
-}
 
 // Round 1 with a wider Z-window: ub[s] = the smallest upper bound of |s - t| over
 // the slots t within +-W of s (singletons: no labels, no atomics).  The points of

@@ -642,19 +642,13 @@ void prepare_bounds(emst_context* c, long long n, bool bounds, double* ms_bounds
       else launch(c, k_seed_round1<2>, grid_for(n, 256), 256, 0, (const float4*)c->spts.p, n, c->core, c->ub.p);
     }
   } else {
-    // ranks of a multi-GPU solve seed only their own Morton range (below), so the scan then
-    // just counts the boundaries
+    // ranks of a multi-GPU solve seed only the boundary pairs of their own Morton range [r0, r1)
     // (exact weights for the building block compute_upper_bounds, round 0; upper bounds in the solve)
     // (the window's pairs include every boundary pair (s, s + 1): with the window on, the
     // scan only counts the boundaries)
-    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim,
-                               bounds && !sharded && !window, c->core, c->round == 0},
+    run_scan(c, n, RoundScanOp{c->label.p, c->spts.p, c->ub.p, c->bprefix.p, n, c->dim, bounds && !window, c->core,
+                               c->round == 0, r0, r1},
              false);
-  }
-  if (sharded && !window && r1 > r0) {
-    const unsigned g = grid_for((r1 - r0 + kScanItems - 1) / kScanItems, kScanThreads);
-    if (c->dim == 3) launch(c, k_seed_boundary<3>, g, kScanThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, r0, r1, c->core, c->ub.p);
-    else launch(c, k_seed_boundary<2>, g, kScanThreads, 0, (const int*)c->label.p, (const float4*)c->spts.p, n, r0, r1, c->core, c->ub.p);
   }
   if (window) {
     const int W = std::min(c->seed_window, kSeedMaxW);
