@@ -1458,17 +1458,17 @@ int boruvka_impl(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
           CK(cudaMemcpyAsync(weights_out, wdst, ne * sizeof(double), cudaMemcpyDeviceToHost, c->copy_stream));
         }
         int64_t* eo = edges_out;
-        CK(c->stager.d2h(edst, (size_t)ne, sizeof(unsigned long long), c->stream,
-                         [eo](size_t at, const unsigned char* src, size_t cnt) {
-                           emst_host::widen_pairs(reinterpret_cast<const unsigned long long*>(src), cnt, eo + 2 * at);
-                         }));
-        if (w_direct) {
-          CK(cudaStreamSynchronize(c->copy_stream));
-        } else {
-          double* wo = weights_out;
-          CK(c->stager.d2h(wdst, (size_t)ne, sizeof(double), c->stream,
-                           [wo](size_t at, const unsigned char* src, size_t cnt) { memcpy(wo + at, src, cnt * 8); }));
-        }
+        double* wo = weights_out;
+        std::vector<emst_host::Stager::Out> outs;
+        outs.push_back({edst, (size_t)ne, sizeof(unsigned long long),
+                        [eo](size_t at, const unsigned char* src, size_t cnt) {
+                          emst_host::widen_pairs(reinterpret_cast<const unsigned long long*>(src), cnt, eo + 2 * at);
+                        }});
+        if (!w_direct)
+          outs.push_back({wdst, (size_t)ne, sizeof(double),
+                          [wo](size_t at, const unsigned char* src, size_t cnt) { memcpy(wo + at, src, cnt * 8); }});
+        CK(c->stager.d2h(outs, c->stream));
+        if (w_direct) CK(cudaStreamSynchronize(c->copy_stream));
         st->d2h_bytes += ne * (sizeof(unsigned long long) + sizeof(double));
       } else if (host_out) {
         CK(cudaMemcpyAsync(edges_out, edst, 2 * ne * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));

@@ -137,11 +137,12 @@ inline bool is_pinned(const void* p) {
 
 // The staging ring and its pool, one per context.
 struct Stager {
-  static constexpr int kSlots = 4;
+  static constexpr int kMaxSlots = 16;
+  int kSlots = 4;                  // (EMST_STAGE_SLOTS)
   size_t kSlotBytes = 16u << 20;   // (EMST_STAGE_MB)
   ThreadPool* pool = nullptr;
-  unsigned char* slot[kSlots] = {};
-  cudaEvent_t ev[kSlots] = {};
+  unsigned char* slot[kMaxSlots] = {};
+  cudaEvent_t ev[kMaxSlots] = {};
   bool ready = false;
 
   cudaError_t init() {
@@ -150,6 +151,7 @@ struct Stager {
     int threads = (int)std::min<unsigned>(hw ? hw : 4, 16u);
     if (const char* t = getenv("EMST_STAGE_THREADS")) threads = std::max(1, atoi(t));
     if (const char* t = getenv("EMST_STAGE_MB")) kSlotBytes = (size_t)std::max(1, atoi(t)) << 20;
+    if (const char* t = getenv("EMST_STAGE_SLOTS")) kSlots = std::min(kMaxSlots, std::max(2, atoi(t)));
     int workers = threads - 1;
     pool = new ThreadPool(std::max(workers, 0));
     for (int i = 0; i < kSlots; ++i) {
@@ -162,7 +164,7 @@ struct Stager {
     return cudaSuccess;
   }
   void release() {
-    for (int i = 0; i < kSlots; ++i) {
+    for (int i = 0; i < kMaxSlots; ++i) {
       if (slot[i]) cudaFreeHost(slot[i]);
       if (ev[i]) cudaEventDestroy(ev[i]);
       slot[i] = nullptr;
@@ -202,35 +204,47 @@ struct Stager {
     return cudaSuccess;   // (later uses of the slots are ordered behind these copies on `s`)
   }
 
-  // device -> host through the ring: `unit` bytes per element on the device, `put(dst_index, slot_ptr,
-  // count)` turns `count` staged elements into the caller's layout (widening or copying)
-  template <class Put>
-  cudaError_t d2h(const void* dev, size_t count, size_t unit, cudaStream_t s, Put put) {
-    const size_t per = kSlotBytes / unit;
-    const size_t chunks = (count + per - 1) / per;
+  // One device -> host stream: `unit` bytes per element on the device, `put(dst_index, slot_ptr, count)`
+  // turns `count` staged elements into the caller's layout (widening or copying).
+  struct Out {
+    const void* dev;
+    size_t count, unit;
+    std::function<void(size_t, const unsigned char*, size_t)> put;
+  };
+
+  // device -> host through the ring, the streams' chunks back to back in one pipeline (the copy
+  // engine does not drain between two outputs)
+  cudaError_t d2h(const std::vector<Out>& outs, cudaStream_t s) {
+    struct Chunk { const Out* o; size_t a, len; };
+    std::vector<Chunk> ch;
+    for (const Out& o : outs) {
+      const size_t per = kSlotBytes / o.unit;
+      for (size_t a = 0; a < o.count; a += per) ch.push_back({&o, a, std::min(per, o.count - a)});
+    }
     auto issue = [&](size_t i) -> cudaError_t {
       const int k = (int)(i % kSlots);
-      const size_t a = i * per, len = std::min(per, count - a);
-      cudaError_t e = cudaMemcpyAsync(slot[k], (const char*)dev + a * unit, len * unit, cudaMemcpyDeviceToHost, s);
+      const Chunk& c = ch[i];
+      cudaError_t e = cudaMemcpyAsync(slot[k], (const char*)c.o->dev + c.a * c.o->unit, c.len * c.o->unit,
+                                      cudaMemcpyDeviceToHost, s);
       if (e != cudaSuccess) return e;
       return cudaEventRecord(ev[k], s);
     };
-    for (size_t i = 0; i < chunks && i < (size_t)kSlots; ++i) {
+    for (size_t i = 0; i < ch.size() && i < (size_t)kSlots; ++i) {
       cudaError_t e = issue(i);
       if (e != cudaSuccess) return e;
     }
-    for (size_t i = 0; i < chunks; ++i) {
+    for (size_t i = 0; i < ch.size(); ++i) {
       const int k = (int)(i % kSlots);
       cudaError_t e = cudaEventSynchronize(ev[k]);
       if (e != cudaSuccess) return e;
-      const size_t a = i * per, len = std::min(per, count - a);
-      const int parts = (int)std::min<size_t>((size_t)pool->size(), std::max<size_t>(1, len >> 17));
-      const size_t step = (len + parts - 1) / parts;
+      const Chunk& c = ch[i];
+      const int parts = (int)std::min<size_t>((size_t)pool->size(), std::max<size_t>(1, c.len >> 17));
+      const size_t step = (c.len + parts - 1) / parts;
       pool->run(parts, [&](int p) {
-        const size_t b = (size_t)p * step, c = std::min(len, b + step);
-        if (b < c) put(a + b, slot[k] + b * unit, c - b);
+        const size_t b = (size_t)p * step, d = std::min(c.len, b + step);
+        if (b < d) c.o->put(c.a + b, slot[k] + b * c.o->unit, d - b);
       });
-      if (i + kSlots < chunks) {
+      if (i + kSlots < ch.size()) {
         e = issue(i + kSlots);
         if (e != cudaSuccess) return e;
       }
