@@ -937,9 +937,11 @@ __global__ void k_edge_w_keys(const EdgeKey* __restrict__ eout, const unsigned* 
 // k_edge_ties) is put in exact (w, uv) order here: its first position takes the
 // smaller of the two records, its second the larger (the partner's record by
 // shuffle, or loaded at a warp edge).  All lanes of the warp must call it.
+// (i1: the end of the launch's positions, <= ne; a partner outside [i0, i1) is loaded)
 __device__ __forceinline__ EdgeKey final_record(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout,
-                                                const unsigned* __restrict__ key, long long ne, long long i) {
-  const bool valid = i < ne;
+                                                const unsigned* __restrict__ key, long long ne, long long i,
+                                                long long i0, long long i1) {
+  const bool valid = i < i1;
   EdgeKey e;
   e.w = ~0ull;
   e.uv = ~0ull;
@@ -959,10 +961,10 @@ __device__ __forceinline__ EdgeKey final_record(const unsigned* __restrict__ ord
   dn.w = __shfl_up_sync(0xffffffffu, e.w, 1);
   dn.uv = __shfl_up_sync(0xffffffffu, e.uv, 1);
   if (side == 1) {
-    const EdgeKey p = lane == 31 ? eout[order[i + 1]] : up;
+    const EdgeKey p = lane == 31 || i + 1 >= i1 ? eout[order[i + 1]] : up;
     if (wuv_less(p, e)) e = p;
   } else if (side == -1) {
-    const EdgeKey p = lane == 0 ? eout[order[i - 1]] : dn;
+    const EdgeKey p = lane == 0 || i - 1 < i0 ? eout[order[i - 1]] : dn;
     if (wuv_less(e, p)) e = p;
   }
   return e;
@@ -973,19 +975,21 @@ __global__ void k_edge_emit(const unsigned* __restrict__ order, const EdgeKey* _
                             const unsigned* __restrict__ key, long long ne, long long* __restrict__ edges,
                             double* __restrict__ weights) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const EdgeKey e = final_record(order, eout, key, ne, i);
+  const EdgeKey e = final_record(order, eout, key, ne, i, 0, ne);
   if (i >= ne) return;
   reinterpret_cast<longlong2*>(edges)[i] = make_longlong2((long long)(e.uv >> 32), (long long)(e.uv & 0xffffffffull));
   weights[i] = __longlong_as_double((long long)e.w);
 }
 
 // the host-pointer entry's variant: packed (u << 32 | v) rows, 8 bytes per edge over PCIe (hostio.h)
+// (positions [i0, i1): the host-output path emits in chunks, each one's copy starting behind it)
 __global__ void k_edge_emit_packed(const unsigned* __restrict__ order, const EdgeKey* __restrict__ eout,
                                    const unsigned* __restrict__ key, long long ne,
-                                   unsigned long long* __restrict__ packed, double* __restrict__ weights) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const EdgeKey e = final_record(order, eout, key, ne, i);
-  if (i >= ne) return;
+                                   unsigned long long* __restrict__ packed, double* __restrict__ weights,
+                                   long long i0, long long i1) {
+  const long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const EdgeKey e = final_record(order, eout, key, ne, i, i0, i1);
+  if (i >= i1) return;
   packed[i] = e.uv;
   weights[i] = __longlong_as_double((long long)e.w);
 }

@@ -183,6 +183,13 @@ struct emst_context {
   DevBuf<int2> tie_runs, tie_mid;   // (start, length) of the longer / 3..32-edge equal-weight runs
   long long* host_counters = nullptr;   // pinned mirror of `counters`
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // deferred final emit (packed host output, EMST_EMIT_OVERLAP): the final order and its keys, and
+  // one event per emitted chunk for the copies to wait on
+  bool emit_overlap = true;
+  bool emit_deferred = false;
+  const unsigned* emit_order = nullptr;
+  const unsigned* emit_key = nullptr;
+  std::vector<cudaEvent_t> emit_ev;
   // Phase timers read back lazily: event pairs are recorded on the stream and
   // their times collected at the next stream sync the solve needs anyway (the
   // round's counter read), so timing adds no host round trip of its own.
@@ -888,12 +895,13 @@ void emit_edges(emst_context* c, const unsigned* order, const unsigned* key, lon
                 double* w_dst, bool packed) {
   if (packed)
     launch(c, k_edge_emit_packed, grid_for(ne, 256), 256, 0, order, (const EdgeKey*)c->eout.p, key, ne,
-           reinterpret_cast<unsigned long long*>(edges_dst), w_dst);
+           reinterpret_cast<unsigned long long*>(edges_dst), w_dst, 0ll, ne);
   else
     launch(c, k_edge_emit, grid_for(ne, 256), 256, 0, order, (const EdgeKey*)c->eout.p, key, ne, edges_dst, w_dst);
 }
 
-void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* w_dst, bool packed = false) {
+void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* w_dst, bool packed = false,
+                   bool defer_emit = false) {
   if (ne <= 0) return;
   unsigned* key = reinterpret_cast<unsigned*>(c->k0.p);
   c->sort_misc.ensure(16);
@@ -928,6 +936,11 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
   CK(cudaFuncSetAttribute(k_edge_fix_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEdgeFixSmem));
   launch(c, k_edge_fix_long, (unsigned)c->num_sms, 1024, kEdgeFixSmem, (const int2*)c->tie_runs.p,
          (const unsigned*)tie + 1, (const EdgeKey*)c->eout.p, order);
+  if (defer_emit) {   // (the host-output path emits chunk by chunk behind its copies: emit_chunked)
+    c->emit_order = order;
+    c->emit_key = kin;
+    return;
+  }
   emit_edges(c, order, kin, ne, edges_dst, w_dst, packed);
 }
 
@@ -1151,8 +1164,11 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     if (st->num_counts < 64) st->component_counts[st->num_counts++] = comps;
   }
   if (edges != n - 1) fail(EMST_ERR_COUNT, "collected %lld edges for %lld points", edges, n);
-  sort_and_emit(c, edges, edges_dev, w_dev, packed);
-  total_weight(c, w_dev, edges, st);
+  // packed host output: the emit and the total are left to emit_chunked, behind which the copies start
+  const bool defer = packed && c->emit_overlap;
+  c->emit_deferred = false;
+  sort_and_emit(c, edges, edges_dev, w_dev, packed, defer);
+  if (!defer) total_weight(c, w_dev, edges, st);
   CK(cudaEventRecord(t2, c->stream));
   CK(cudaEventSynchronize(t2));
   read_counters(c);
@@ -1162,6 +1178,8 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
     CK(cudaEventRecord(t2, c->stream));
     CK(cudaEventSynchronize(t2));
     read_counters(c);
+  } else if (defer) {
+    c->emit_deferred = true;
   }
   long long evals = c->host_counters[0];
   if (c->world > 1) {
@@ -1286,6 +1304,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     if (const char* t = getenv("EMST_LIST_SKIP")) c->list_skip = atof(t);
     if (const char* t = getenv("EMST_SINGLE_KERNEL")) c->single_kernel = atoi(t) != 0;
     if (const char* t = getenv("EMST_STAGE")) c->staging = atoi(t) != 0;
+    if (const char* t = getenv("EMST_EMIT_OVERLAP")) c->emit_overlap = atoi(t) != 0;
     if (const char* t = getenv("EMST_PACKED")) c->packed_out = atoi(t) != 0;
     c->rank = rank;
     c->world = world;
@@ -1331,6 +1350,8 @@ int emst_context_destroy(emst_context* c) {
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
+  for (cudaEvent_t e : c->emit_ev) cudaEventDestroy(e);
+  c->emit_ev.clear();
   for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1452,10 +1473,35 @@ int boruvka_impl(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
         // (u << 32 | v) rows widened on the host while the next chunk is in flight (hostio.h)
         CK(c->stager.init());
         const bool w_direct = emst_host::is_pinned(weights_out);
+        const bool chunked = c->emit_deferred;
+        // chunked: the final emit runs chunk by chunk on the compute stream, each chunk's copy waits
+        // only for its own emit (copy stream), and the total weight follows the last chunk
+        const size_t per = c->stager.kSlotBytes / sizeof(unsigned long long);
+        const cudaEvent_t* ready = nullptr;
+        if (chunked) {
+          const long long chunks = (ne + (long long)per - 1) / (long long)per;
+          while ((long long)c->emit_ev.size() < chunks) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            c->emit_ev.push_back(e);
+          }
+          for (long long k = 0; k < chunks; ++k) {
+            const long long i0 = k * (long long)per, i1 = std::min<long long>(ne, i0 + (long long)per);
+            launch(c, k_edge_emit_packed, grid_for(i1 - i0, 256), 256, 0, c->emit_order, (const EdgeKey*)c->eout.p,
+                   c->emit_key, ne, reinterpret_cast<unsigned long long*>(edst), wdst, i0, i1);
+            CK(cudaEventRecord(c->emit_ev[k], c->stream));
+          }
+          total_weight(c, wdst, ne, st);
+          ready = c->emit_ev.data();
+        }
         if (w_direct) {   // page-locked destination: straight DMA, concurrent with the edge chunks below
-          CK(cudaEventRecord(c->ev_b, c->stream));
-          CK(cudaStreamWaitEvent(c->copy_stream, c->ev_b, 0));
-          CK(cudaMemcpyAsync(weights_out, wdst, ne * sizeof(double), cudaMemcpyDeviceToHost, c->copy_stream));
+          if (chunked) {
+            CK(cudaMemcpyAsync(weights_out, wdst, ne * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+          } else {
+            CK(cudaEventRecord(c->ev_b, c->stream));
+            CK(cudaStreamWaitEvent(c->copy_stream, c->ev_b, 0));
+            CK(cudaMemcpyAsync(weights_out, wdst, ne * sizeof(double), cudaMemcpyDeviceToHost, c->copy_stream));
+          }
         }
         int64_t* eo = edges_out;
         double* wo = weights_out;
@@ -1463,12 +1509,19 @@ int boruvka_impl(emst_context* c, const float* pts, int64_t n, int32_t d, int32_
         outs.push_back({edst, (size_t)ne, sizeof(unsigned long long),
                         [eo](size_t at, const unsigned char* src, size_t cnt) {
                           emst_host::widen_pairs(reinterpret_cast<const unsigned long long*>(src), cnt, eo + 2 * at);
-                        }});
+                        },
+                        ready, per});
         if (!w_direct)
           outs.push_back({wdst, (size_t)ne, sizeof(double),
-                          [wo](size_t at, const unsigned char* src, size_t cnt) { memcpy(wo + at, src, cnt * 8); }});
-        CK(c->stager.d2h(outs, c->stream));
-        if (w_direct) CK(cudaStreamSynchronize(c->copy_stream));
+                          [wo](size_t at, const unsigned char* src, size_t cnt) { memcpy(wo + at, src, cnt * 8); },
+                          ready, per});
+        CK(c->stager.d2h(outs, chunked ? c->copy_stream : c->stream));
+        if (chunked) {
+          c->emit_deferred = false;
+          CK(cudaStreamSynchronize(c->copy_stream));   // (c->stream is synchronised below)
+        } else if (w_direct) {
+          CK(cudaStreamSynchronize(c->copy_stream));
+        }
         st->d2h_bytes += ne * (sizeof(unsigned long long) + sizeof(double));
       } else if (host_out) {
         CK(cudaMemcpyAsync(edges_out, edst, 2 * ne * sizeof(long long), cudaMemcpyDeviceToHost, c->stream));

@@ -210,6 +210,8 @@ struct Stager {
     const void* dev;
     size_t count, unit;
     std::function<void(size_t, const unsigned char*, size_t)> put;
+    const cudaEvent_t* ready = nullptr;   // optional: ready[e / ready_per] is recorded once element e exists
+    size_t ready_per = 0;
   };
 
   // device -> host through the ring, the streams' chunks back to back in one pipeline (the copy
@@ -224,6 +226,10 @@ struct Stager {
     auto issue = [&](size_t i) -> cudaError_t {
       const int k = (int)(i % kSlots);
       const Chunk& c = ch[i];
+      if (c.o->ready) {   // wait for the producer of the chunk's last element
+        cudaError_t e = cudaStreamWaitEvent(s, c.o->ready[(c.a + c.len - 1) / c.o->ready_per], 0);
+        if (e != cudaSuccess) return e;
+      }
       cudaError_t e = cudaMemcpyAsync(slot[k], (const char*)c.o->dev + c.a * c.o->unit, c.len * c.o->unit,
                                       cudaMemcpyDeviceToHost, s);
       if (e != cudaSuccess) return e;
