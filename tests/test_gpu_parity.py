@@ -331,11 +331,13 @@ def test_merge_components_rejects_bad_state():
                            E.OutgoingEdges(out.reps, oob, out.v, out.w, 0))
 
 
-@pytest.mark.parametrize("env", [{}, {"EMST_STAGE": "0"}, {"EMST_PACKED": "0"}])
+@pytest.mark.parametrize("env", [{}, {"EMST_STAGE": "0"}, {"EMST_PACKED": "0"}, {"EMST_STAGE_MB": "1"},
+                                 {"EMST_EMIT_OVERLAP": "0"}])
 def test_host_transfer_paths(large_golden, env, monkeypatch):
     """The host-pointer entry's transfer variants (hostio.h): staged pageable input or plain cudaMemcpy,
     packed (u << 32 | v) rows widened on the host or int64 rows from the device, weights straight into a
-    page-locked buffer or through the staging ring, 16-byte aligned or unaligned int64 rows."""
+    page-locked buffer or through the staging ring, 16-byte aligned or unaligned int64 rows, the final
+    emit in chunks behind their copies (1-MB slots: 8 chunks here) or in one launch."""
     import ctypes
     import torch
     from paper_2207_00514_b200 import _lib
@@ -396,3 +398,32 @@ def test_equal_sort_keys_order_exactly(d, jitter):
     assert np.count_nonzero(inside) > 100   # runs of equal keys with distinct weights do occur
     assert np.array_equal(res.edges, ref.edges) and np.array_equal(res.weights, ref.weights)
     assert res.total_weight == ref.total_weight
+
+
+def test_chunked_emit_orders_ties_across_chunk_boundaries(monkeypatch):
+    """The host-output path emits the final order in chunks (one per staging slot, 131072 edges with
+    1-MB slots) and orders each run of exactly two equal sort keys inside the emit, loading the partner
+    record when it lies in the neighbouring chunk.  A jittered lattice has such runs everywhere; the
+    result must equal the device-output path, which emits in one launch."""
+    import torch
+    monkeypatch.setenv("EMST_STAGE_MB", "1")
+    rng = np.random.default_rng(5)
+    side = 56
+    g = np.arange(side, dtype=np.float64) * 65536
+    lat = np.stack(np.meshgrid(g, g, g, indexing="ij"), -1).reshape(-1, 3)
+    pts = (lat + rng.uniform(-0.5, 0.5, lat.shape)).astype(np.float32)
+    pts = np.concatenate([pts, np.full((1, 3), 1e18, np.float32)])
+    ctx = E.Context(0)
+    try:
+        res = E.boruvka_emst(pts, context=ctx)
+    finally:
+        ctx.close()
+    n = pts.shape[0]
+    e = torch.empty((n - 1, 2), dtype=torch.int64, device="cuda")
+    w = torch.empty((n - 1,), dtype=torch.float64, device="cuda")
+    E.boruvka_emst_device(torch.from_numpy(pts).cuda(), e, w)
+    assert np.array_equal(res.edges, e.cpu().numpy()) and np.array_equal(res.weights, w.cpu().numpy())
+    keys = _sort_key32(res.weights)
+    per = (1 << 20) // 8
+    at = np.arange(per, n - 1, per)
+    assert np.count_nonzero(keys[at - 1] == keys[at]) > 0   # equal keys do straddle a chunk boundary
