@@ -731,6 +731,7 @@ __global__ void k_fold_rows(unsigned long long* __restrict__ buf, int rows, long
 // Edges live as one 16-byte record (uv, w) so that every gather is one sector.
 constexpr int kThreadTie = 8;     // tie runs up to this long are ordered in registers by one thread
 constexpr int kShortTie = 32;     // ... up to this long by one warp each
+constexpr int kSmallTie = 256;    // ... up to this long by one 128-thread block each (small shared footprint)
 constexpr int kBlockTie = 4096;   // longer ones up to this long by one block each
 
 // range[0] = min, range[1] = max of the weight bits (range preset to (~0, 0))
@@ -779,7 +780,8 @@ __device__ __forceinline__ bool wuv_less(const EdgeKey& a, const EdgeKey& b) {
 // two-key sort.
 __global__ void k_edge_ties(const unsigned* __restrict__ key, long long ne, const EdgeKey* __restrict__ eout,
                             unsigned* __restrict__ order, unsigned* __restrict__ max_run, int2* __restrict__ runs,
-                            unsigned* __restrict__ run_count, int2* __restrict__ mid, unsigned* __restrict__ mid_count) {
+                            unsigned* __restrict__ run_count, int2* __restrict__ mid, unsigned* __restrict__ mid_count,
+                            int2* __restrict__ small, unsigned* __restrict__ small_count) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   int len = 0;
   if (i + 1 < ne) {
@@ -825,8 +827,10 @@ __global__ void k_edge_ties(const unsigned* __restrict__ key, long long ne, cons
     for (int a = 0; a < kThreadTie; ++a) if (a < len) order[i + a] = o[a];
   } else if (len > kBlockTie) {
     atomicMax(max_run, (unsigned)len);   // (only the overflow matters to the host)
-  } else if (len > kShortTie) {
+  } else if (len > kSmallTie) {
     runs[atomicAdd(run_count, 1u)] = make_int2((int)i, len);
+  } else if (len > kShortTie) {
+    small[atomicAdd(small_count, 1u)] = make_int2((int)i, len);
   }
   // runs of kThreadTie+1..kShortTie: one list append per warp
   const bool is_mid = len > kThreadTie && len <= kShortTie;
@@ -877,7 +881,50 @@ __global__ void k_edge_fix_mid(const int2* __restrict__ mid, const unsigned* __r
   }
 }
 
-// One block per listed run (kShortTie < length <= kBlockTie; grid-stride over
+// One 128-thread block per listed run of kShortTie+1..kSmallTie edges (grid-stride over the
+// device-side count): the same bitonic sort as k_edge_fix_long in 5 KB of shared memory, so many
+// blocks share an SM and a short run does not hold a 1024-thread block through its barriers.
+constexpr int kSmallTieThreads = 128;
+__global__ void __launch_bounds__(kSmallTieThreads) k_edge_fix_small(const int2* __restrict__ runs,
+                                                                     const unsigned* __restrict__ run_count,
+                                                                     const EdgeKey* __restrict__ eout,
+                                                                     unsigned* __restrict__ order) {
+  __shared__ EdgeKey sk[kSmallTie];
+  __shared__ unsigned so[kSmallTie];
+  const unsigned cnt = *run_count;
+  for (unsigned ri = blockIdx.x; ri < cnt; ri += gridDim.x) {
+    const int2 r = runs[ri];
+    int size = 1;
+    while (size < r.y) size <<= 1;
+    for (int a = threadIdx.x; a < size; a += blockDim.x) {
+      const unsigned o = a < r.y ? order[r.x + a] : 0u;
+      so[a] = o;
+      if (a < r.y) sk[a] = eout[o];
+      else { sk[a].w = ~0ull; sk[a].uv = ~0ull; }
+    }
+    __syncthreads();
+    for (int k = 2; k <= size; k <<= 1) {
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        for (int a = threadIdx.x; a < size; a += blockDim.x) {
+          const int b = a ^ j;
+          if (b > a) {
+            const bool up = (a & k) == 0;
+            const EdgeKey ka = sk[a], kb = sk[b];
+            if (wuv_less(kb, ka) == up) {
+              sk[a] = kb; sk[b] = ka;
+              const unsigned t = so[a]; so[a] = so[b]; so[b] = t;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int a = threadIdx.x; a < r.y; a += blockDim.x) order[r.x + a] = so[a];
+    __syncthreads();   // (the shared arrays are reused by the next run)
+  }
+}
+
+// One block per listed run (kSmallTie < length <= kBlockTie; grid-stride over
 // the device-side count): bitonic sort of the run's ((w, uv), edge) triples in
 // shared memory (dynamic, kEdgeFixSmem bytes).
 constexpr size_t kEdgeFixSmem = (size_t)kBlockTie * (16 + 4);

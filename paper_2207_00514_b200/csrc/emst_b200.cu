@@ -180,7 +180,7 @@ struct emst_context {
   DevBuf<long long> out_edges;
   DevBuf<double> out_w;
   DevBuf<double> pairwise;   // total-weight partial sums
-  DevBuf<int2> tie_runs, tie_mid;   // (start, length) of the longer / 3..32-edge equal-weight runs
+  DevBuf<int2> tie_runs, tie_mid, tie_small;   // (start, length) of the 257..4096 / 9..32 / 33..256-edge equal-key runs
   long long* host_counters = nullptr;   // pinned mirror of `counters`
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
   // deferred final emit (packed host output, EMST_EMIT_OVERLAP): the final order and its keys, and
@@ -928,11 +928,15 @@ void sort_and_emit(emst_context* c, long long ne, long long* edges_dst, double* 
   unsigned* mid_n = reinterpret_cast<unsigned*>(dev_counter(c, 11));
   CK(cudaMemsetAsync(mid_n, 0, sizeof(long long), c->stream));
   c->tie_mid.ensure(ne / (kThreadTie + 1) + 1);
+  c->tie_small.ensure(ne / (kShortTie + 1) + 1);
+  unsigned* small_n = mid_n + 1;   // (high word of counters[11])
   launch(c, k_edge_ties, grid_for(ne, 256), 256, 0, (const unsigned*)kin, ne, (const EdgeKey*)c->eout.p, order,
-         (unsigned*)tie, c->tie_runs.p, (unsigned*)tie + 1, c->tie_mid.p, mid_n);
+         (unsigned*)tie, c->tie_runs.p, (unsigned*)tie + 1, c->tie_mid.p, mid_n, c->tie_small.p, small_n);
   // (grids sized for the worst case; the kernels stride over the device-side counts)
   launch(c, k_edge_fix_mid, (unsigned)c->num_sms * 8, 256, 0, (const int2*)c->tie_mid.p, (const unsigned*)mid_n,
          (const EdgeKey*)c->eout.p, order);
+  launch(c, k_edge_fix_small, (unsigned)c->num_sms * 8, kSmallTieThreads, 0, (const int2*)c->tie_small.p,
+         (const unsigned*)small_n, (const EdgeKey*)c->eout.p, order);
   CK(cudaFuncSetAttribute(k_edge_fix_long, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kEdgeFixSmem));
   launch(c, k_edge_fix_long, (unsigned)c->num_sms, 1024, kEdgeFixSmem, (const int2*)c->tie_runs.p,
          (const unsigned*)tie + 1, (const EdgeKey*)c->eout.p, order);
@@ -1191,9 +1195,9 @@ void solve(emst_context* c, const float* dev_pts, long long n, int d, int flags,
   st->leaf_distance_evals = evals;
   if (c->trace) {
     fprintf(stderr, "[emst] merge-to-next-round gaps: %.3f ms in all\n", c->gap_ms);
-    fprintf(stderr, "[emst] final order: longest equal-key run %u, runs of 33..4096: %u, runs of 9..32: %u\n",
+    fprintf(stderr, "[emst] final order: longest equal-key run %u, runs of 257..4096: %u, 33..256: %u, 9..32: %u\n",
             (unsigned)(c->host_counters[7] & 0xffffffffll), (unsigned)((unsigned long long)c->host_counters[7] >> 32),
-            (unsigned)(c->host_counters[11] & 0xffffffffll));
+            (unsigned)((unsigned long long)c->host_counters[11] >> 32), (unsigned)(c->host_counters[11] & 0xffffffffll));
   }
   c->gap_ms = 0.0;
   c->merge_end = nullptr;
@@ -1346,7 +1350,7 @@ int emst_context_destroy(emst_context* c) {
   c->succ.release(); c->ptr.release(); c->root.release(); c->newid.release(); c->fin.release();
   c->eout.release(); c->xw.release(); c->xuv.release(); c->exch_host.release();
   c->stager.release();
-  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release(); c->tie_mid.release();
+  c->scan_scratch.release(); c->counters.release(); c->out_edges.release(); c->out_w.release(); c->pairwise.release(); c->tie_runs.release(); c->tie_mid.release(); c->tie_small.release();
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_b) cudaEventDestroy(c->ev_b);
