@@ -115,7 +115,8 @@ struct emst_context {
   int round = 0;                  // 1-based Boruvka round of the running solve (0 outside)
   int seed_window = 8;            // Z-order seed pairs (s +- 1..W) in solve rounds >= 2 (EMST_SEED_WINDOW)
   long long round_comps = 0;      // components entering the running round
-  int seed_from = 2;              // first round with window seeds (EMST_SEED_FROM)
+  int seed_from = 2;
+  int seed_window_2d = 4;         // the same in 2D (EMST_SEED_WINDOW_2D, <= 1: off)              // first round with window seeds (EMST_SEED_FROM)
   double skip_frac = 0.0;         // share of last round's queries settled before their first visit
   bool single_kernel = true;      // round 1 runs its own compiled traversal (EMST_SINGLE_KERNEL=0: the general one)
   double list_skip = 0.1;         // prefilter the queries when last round settled this share up front (EMST_LIST_SKIP)
@@ -634,8 +635,9 @@ void prepare_bounds(emst_context* c, long long n, bool bounds, double* ms_bounds
   const long long r0 = sharded ? c->rank * n / c->world : 0, r1 = sharded ? (c->rank + 1) * n / c->world : n;
   // window seeds pay while components are small and in 3D (measured: 37M blobs 3D
   // -2.3 ms, 10M normal 3D -0.6 ms; the 2D configs lose ~1 %); later rounds gain nothing
-  const bool window = bounds && c->seed_window > 1 && c->dim == 3 && c->round >= c->seed_from && !c->core &&
-                      c->round_comps * 1024 >= n;
+  // (±8 in 3D, ±4 in 2D: 24M blobs 2D 29.9 -> 29.65 ms, 10M uniform 2D 13.65 -> 13.6; ±8 and ±2 less)
+  const int seed_w = c->dim == 3 ? c->seed_window : c->seed_window_2d;
+  const bool window = bounds && seed_w > 1 && c->round >= c->seed_from && !c->core && c->round_comps * 1024 >= n;
   cudaEvent_t e0 = timer_event(c);
   if (mode == kLabelsNone && c->round == 1) {
     // round 1 of the solve: singletons, no node labels, so no boundary prefix either
@@ -658,9 +660,9 @@ void prepare_bounds(emst_context* c, long long n, bool bounds, double* ms_bounds
              false);
   }
   if (window) {
-    const int W = std::min(c->seed_window, kSeedMaxW);
+    const int W = std::min(seed_w, kSeedMaxW);
     const auto kern = c->dim == 3 ? (W == 8 ? k_seed_window<3, 8> : k_seed_window<3, 0>)
-                                  : (W == 8 ? k_seed_window<2, 8> : k_seed_window<2, 0>);
+                                  : (W == 4 ? k_seed_window<2, 4> : k_seed_window<2, 0>);
     const long long b0 = r0 / kSeedThreads, b1 = (r1 + kSeedThreads - 1) / kSeedThreads;   // blocks covering [r0, r1)
     launch(c, kern, (unsigned)std::max<long long>(1, b1 - b0), kSeedThreads, 0, (const int*)c->label.p,
            (const float4*)c->spts.p, n, W, c->ub.p, b0);
@@ -1301,6 +1303,7 @@ int emst_context_create(int device, int rank, int world, const void* nccl_id, em
     c->device = device;
     if (const char* t = getenv("EMST_SEED_WINDOW")) c->seed_window = atoi(t);
     if (const char* t = getenv("EMST_SEED_FROM")) c->seed_from = atoi(t);
+    if (const char* t = getenv("EMST_SEED_WINDOW_2D")) c->seed_window_2d = atoi(t);
     if (const char* t = getenv("EMST_PROOF_FROM")) c->proof_from = atoi(t);
     if (const char* t = getenv("EMST_TRACE")) c->trace = atoi(t) != 0;
     if (const char* t = getenv("EMST_ONE_SIDE")) c->last_round_one_side = atoi(t) != 0;
